@@ -1,0 +1,624 @@
+// kernels.cuh -- sm_100a device code of the MBP decoder.
+//
+// Layout ("frame-interleaved", lane = frame): frames are processed in groups
+// of 32; group g's per-edge message for edge e lives in one 128-byte line
+// c2v[(g*E + e)*32 + lane] (256 B in fp64 mode), its posterior for variable i
+// in post[(g*n + i)*32 + lane].  A warp therefore updates one check (or one
+// variable) for 32 frames at once: the graph indices it reads are
+// warp-uniform, every message access is one fully used, coalesced line, and
+// rows of different degree never diverge a warp.  Bits (noisy key, hard
+// decision, syndrome) are 32-frame words: word[g*n + i] bit f = frame 32g+f.
+//
+// One persistent cooperative kernel runs the whole flooding decode
+// (decode_loop, _kernels.py:323-379): per sweep a check phase (Eq. 6,
+// c2v_pass _kernels.py:230-261, with the variable-to-check message formed on
+// the fly in APP form v2c = clamp(post - c2v), exact because the reference's
+// joint `total` IS the posterior sum, _kernels.py:276-279 vs 296-300), a
+// variable phase (posterior Eq. 2 + hard decision, _kernels.py:293-307), and
+// a syndrome phase (mismatch_count, _kernels.py:310-320) whose per-frame
+// counts drive early termination; phases are separated by a grid barrier.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mbp {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kMaxU = 16;
+
+// ---------------------------------------------------------------------------
+// cache-control loads.  Messages and bit words are rewritten by other SMs
+// between phases of the same launch, so they are read L2-coherent (.cg,
+// never from a possibly stale L1 line); graph indices are immutable (.nc).
+// ---------------------------------------------------------------------------
+template <class T> __device__ __forceinline__ T ld_cg(const T* p) { return __ldcg(p); }
+template <class T> __device__ __forceinline__ T ld_ro(const T* p) { return __ldg(p); }
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p)
+{
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Grid-wide barrier for a cooperatively launched (co-resident) grid.
+// bar[0] = arrival count, bar[1] = generation.
+__device__ __forceinline__ void grid_barrier(unsigned* bar)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned gen = ld_acquire(bar + 1);
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            bar[0] = 0;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (ld_acquire(bar + 1) == gen) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Eq. 6 in the phi domain (fp32).  phi(x) = -ln tanh(x/2) = log1p(2/expm1(x))
+// is an involution on [0, inf]; for the other-edge set N(j)\a,
+//   |2 atanh(prod tanh(x_b/2))| = phi( sum phi(|x_b|) ),
+//   sign = prod sign(x_b).
+// Exclusive sums come from prefix + suffix sums (no total-minus-own
+// cancellation; phi(0) = inf propagates to an exact 0 output).  |x| >= sat
+// contributes phi = 0: that is where the reference's float64 tanh(x/2)
+// rounds to exactly 1.0, and all-others-saturated then gives +-clamp as in
+// the `prod >= 1.0` branch of c2v_pass (_kernels.py:249-252).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float phi_f32(float x)
+{
+    return log1pf(2.0f / expm1f(x));
+}
+
+template <int D> struct SignMask { using T = unsigned; };
+template <> struct SignMask<64> { using T = unsigned long long; };
+
+template <int D>
+__device__ __forceinline__ void c2v_rule(const float (&x)[D], int d, unsigned flip, float clamp,
+                                         float sat, float (&out)[D])
+{
+    using M = typename SignMask<D>::T;
+    float ph[D];
+    M sg = 0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        ph[k] = 0.0f;
+        if (k < d) {
+            const float a = fabsf(x[k]);
+            ph[k] = a >= sat ? 0.0f : phi_f32(a);
+            sg |= (M)(x[k] < 0.0f) << k;
+        }
+    }
+    float suf[D];
+    float s = 0.0f;
+#pragma unroll
+    for (int k = D - 1; k >= 0; --k) {
+        suf[k] = s;
+        s += ph[k];
+    }
+    const unsigned par = (sizeof(M) == 8 ? __popcll((unsigned long long)sg) : __popc((unsigned)sg)) & 1u;
+    float pre = 0.0f;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        if (k < d) {
+            const float ex = pre + suf[k];
+            pre += ph[k];
+            const float mag = fminf(phi_f32(ex), clamp);
+            const unsigned neg = par ^ (unsigned)((sg >> k) & 1) ^ flip;
+            out[k] = neg ? -mag : mag;
+        }
+    }
+}
+
+// Eq. 6 literally (fp64 parity mode): t_b = tanh(x_b/2), product over the
+// other edges in ascending order with no division (prefix, then the rest in
+// order -- the exact multiplication sequence of c2v_pass), saturation,
+// 2*atanh, syndrome sign, clamp.
+template <int D>
+__device__ __forceinline__ void c2v_rule(const double (&x)[D], int d, unsigned flip, double clamp,
+                                         float /*sat*/, double (&out)[D])
+{
+    double t[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) t[k] = k < d ? tanh(0.5 * x[k]) : 1.0;
+    double pre = 1.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        if (a < d) {
+            double prod = pre;
+#pragma unroll 4
+            for (int b = a + 1; b < D; ++b)
+                if (b < d) prod *= t[b];
+            pre *= t[a];
+            double r = prod >= 1.0 ? clamp : (prod <= -1.0 ? -clamp : 2.0 * atanh(prod));
+            if (flip) r = -r;
+            out[a] = r > clamp ? clamp : (r < -clamp ? -clamp : r);
+        }
+    }
+}
+
+template <class Real> __device__ __forceinline__ Real clampr(Real v, Real c)
+{
+    return v > c ? c : (v < -c ? -c : v);
+}
+
+// ---------------------------------------------------------------------------
+// decode kernel arguments
+// ---------------------------------------------------------------------------
+template <class Real>
+struct DecodeArgs {
+    // graph (stacked, int32 indices)
+    int n, m, u, C, E;
+    const int* __restrict__ chk_ptr;   // [C+1]
+    const int* __restrict__ chk_var;   // [E]
+    const int* __restrict__ var_ptr;   // [n+1]
+    const int* __restrict__ var_edge;  // [E]
+    int edge_off[kMaxU + 1];
+    // batch
+    int G;                       // groups of 32 frames
+    // state
+    Real* __restrict__ c2v;      // [G][E][32]
+    Real* __restrict__ post;     // [G][P][n][32], P = ISO ? u+1 : 1
+    Real* __restrict__ v2c;      // [G][E][32] (damping only)
+    const Real* __restrict__ Lmag;      // [G*32] prior magnitude per frame
+    const unsigned* __restrict__ noisy_w;  // [G][n]
+    const unsigned* __restrict__ syn_w;    // [G][C]
+    unsigned* __restrict__ hard_w;         // [G][n]
+    unsigned* __restrict__ hist_w;         // [(T+1)][G][n] or null
+    int* __restrict__ cnt;       // [2][G*32] mismatch counts by sweep parity
+    int* __restrict__ any_bad;   // [2]
+    int* __restrict__ iters;     // [G*32] first converged sweep, -1 unset
+    unsigned* __restrict__ barrier;  // [2]
+    int* __restrict__ sweeps_run;    // [1]
+    // outputs (per frame, batch B)
+    int B;
+    uint8_t* __restrict__ out_conv;
+    int* __restrict__ out_iters;
+    int* __restrict__ out_mism;
+    // config
+    int max_it;
+    Real clamp;
+    Real damping;
+    float sat;
+};
+
+// Check phase item: check j of group g at sweep t; `act` = lanes (frames)
+// still decoding.  Reads post_{t-1}, c2v_{t-1}, writes c2v_t.
+template <class Real, int D, bool DAMP, bool ISO>
+__device__ __forceinline__ void check_item(const DecodeArgs<Real>& A, int g, int j, int t,
+                                           unsigned act, int lane)
+{
+    const int e0 = ld_ro(A.chk_ptr + j);
+    const int d = ld_ro(A.chk_ptr + j + 1) - e0;
+    constexpr int NC = (D + 31) / 32;
+    int vid[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) vid[c] = (c * 32 + lane < d) ? ld_ro(A.chk_var + e0 + c * 32 + lane) : 0;
+    const bool live = (act >> lane) & 1u;
+    const unsigned flip = (ld_ro(A.syn_w + (size_t)g * A.C + j) >> lane) & 1u;
+    const Real L = ld_ro(A.Lmag + g * 32 + lane);
+    const int mat = ISO ? j / A.m : 0;
+    const size_t lineE = (size_t)g * A.E + e0;
+    const Real* postg = A.post + ((size_t)g * (ISO ? A.u + 1 : 1) + mat) * A.n * 32;
+
+    Real x[D];
+    if (t == 1) {
+        // sweep 1 reads the UNCLAMPED prior (decode_loop init, _kernels.py:353-355)
+        const unsigned* nw = A.noisy_w + (size_t)g * A.n;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            if (k < d) {
+                const int v = __shfl_sync(kFull, vid[k >> 5], k & 31);
+                x[k] = ((ld_ro(nw + v) >> lane) & 1u) ? -L : L;
+            } else {
+                x[k] = Real(0);
+            }
+        }
+        if (DAMP && live) {
+#pragma unroll
+            for (int k = 0; k < D; ++k)
+                if (k < d) A.v2c[(lineE + k) * 32 + lane] = x[k];
+        }
+    } else {
+        Real p[D], q[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            p[k] = Real(0);
+            q[k] = Real(0);
+            if (k < d) {
+                const int v = __shfl_sync(kFull, vid[k >> 5], k & 31);
+                if (live) {
+                    p[k] = ld_cg(postg + (size_t)v * 32 + lane);
+                    q[k] = ld_cg(A.c2v + (lineE + k) * 32 + lane);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            Real val = p[k] - q[k];
+            if (DAMP) {
+                if (k < d && live) {
+                    const Real old = ld_cg(A.v2c + (lineE + k) * 32 + lane);
+                    val = (Real(1) - A.damping) * val + A.damping * old;
+                }
+            }
+            x[k] = clampr(val, A.clamp);
+        }
+        if (DAMP && live) {
+#pragma unroll
+            for (int k = 0; k < D; ++k)
+                if (k < d) A.v2c[(lineE + k) * 32 + lane] = x[k];
+        }
+    }
+    Real out[D];
+    c2v_rule<D>(x, d, flip, A.clamp, A.sat, out);
+    if (live) {
+#pragma unroll
+        for (int k = 0; k < D; ++k)
+            if (k < d) A.c2v[(lineE + k) * 32 + lane] = out[k];
+    }
+}
+
+// Variable phase item: variable i of group g at sweep t.  Joint posterior
+// prior + sum of every matrix's c2v in ascending edge order (posterior_pass);
+// in isolated mode also the per-matrix totals v2c_pass uses
+// (_kernels.py:276-279).  Hard decision post < 0 (ties -> 0) as a ballot.
+template <class Real, bool ISO>
+__device__ __forceinline__ void var_item(const DecodeArgs<Real>& A, int g, int i, int t,
+                                         unsigned act, int lane)
+{
+    const int p0 = ld_ro(A.var_ptr + i);
+    const int dv = ld_ro(A.var_ptr + i + 1) - p0;
+    const bool live = (act >> lane) & 1u;
+    const unsigned nwd = ld_ro(A.noisy_w + (size_t)g * A.n + i);
+    const Real L = ld_ro(A.Lmag + g * 32 + lane);
+    const Real prior = ((nwd >> lane) & 1u) ? -L : L;
+    const Real* c2vg = A.c2v + (size_t)g * A.E * 32 + lane;
+    Real acc = prior;
+    if (!ISO) {
+        for (int base = 0; base < dv; base += 32) {
+            const int eid = base + lane < dv ? ld_ro(A.var_edge + p0 + base + lane) : 0;
+            const int cnt = min(32, dv - base);
+            if (cnt == 6) {  // regular column degree 3 at u = 2: fully unrolled
+                Real c[6];
+#pragma unroll
+                for (int k = 0; k < 6; ++k) {
+                    const int e = __shfl_sync(kFull, eid, k);
+                    c[k] = live ? ld_cg(c2vg + (size_t)e * 32) : Real(0);
+                }
+#pragma unroll
+                for (int k = 0; k < 6; ++k) acc += c[k];
+            } else if (cnt == 9) {  // u = 3
+                Real c[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) {
+                    const int e = __shfl_sync(kFull, eid, k);
+                    c[k] = live ? ld_cg(c2vg + (size_t)e * 32) : Real(0);
+                }
+#pragma unroll
+                for (int k = 0; k < 9; ++k) acc += c[k];
+            } else {
+#pragma unroll 4
+                for (int k = 0; k < cnt; ++k) {
+                    const int e = __shfl_sync(kFull, eid, k);
+                    if (live) acc += ld_cg(c2vg + (size_t)e * 32);
+                }
+            }
+        }
+        if (live) A.post[((size_t)g * A.n + i) * 32 + lane] = acc;
+    } else {
+        const size_t P = (size_t)(A.u + 1);
+        Real part = prior;
+        int l = 0;
+        for (int base = 0; base < dv; base += 32) {
+            const int eid = base + lane < dv ? ld_ro(A.var_edge + p0 + base + lane) : 0;
+            const int cnt = min(32, dv - base);
+            for (int k = 0; k < cnt; ++k) {
+                const int e = __shfl_sync(kFull, eid, k);
+                while (e >= A.edge_off[l + 1]) {  // close the totals of matrices before e's
+                    if (live) A.post[(((size_t)g * P + l) * A.n + i) * 32 + lane] = part;
+                    part = prior;
+                    ++l;
+                }
+                const Real c = live ? ld_cg(c2vg + (size_t)e * 32) : Real(0);
+                acc += c;
+                part += c;
+            }
+        }
+        for (; l < A.u; ++l) {
+            if (live) A.post[(((size_t)g * P + l) * A.n + i) * 32 + lane] = part;
+            part = prior;
+        }
+        if (live) A.post[(((size_t)g * P + A.u) * A.n + i) * 32 + lane] = acc;
+    }
+    const unsigned neg = __ballot_sync(kFull, acc < Real(0));
+    if (lane == 0) {
+        const size_t w = (size_t)g * A.n + i;
+        const unsigned old = ld_cg(A.hard_w + w);
+        const unsigned hw = (neg & act) | (old & ~act);
+        A.hard_w[w] = hw;
+        if (A.hist_w) A.hist_w[((size_t)t * A.G) * A.n + w] = hw;
+    }
+}
+
+// Syndrome phase item: 32 consecutive checks (lane = check) of group g.
+// Mismatch words (bit f = frame f) are turned into per-frame counts with 32
+// ballots and added to cnt[t&1].
+template <class Real>
+__device__ __forceinline__ void syncheck_item(const DecodeArgs<Real>& A, int g, int blk, int t,
+                                              unsigned act, int lane)
+{
+    const int j = blk * 32 + lane;
+    unsigned mism = 0;
+    if (j < A.C) {
+        const unsigned* hw = A.hard_w + (size_t)g * A.n;
+        const int a0 = ld_ro(A.chk_ptr + j), a1 = ld_ro(A.chk_ptr + j + 1);
+        unsigned par = 0;
+        for (int a = a0; a < a1; ++a) par ^= ld_cg(hw + ld_ro(A.chk_var + a));
+        mism = (par ^ ld_ro(A.syn_w + (size_t)g * A.C + j)) & act;
+    }
+    int c = 0;
+#pragma unroll
+    for (int f = 0; f < 32; ++f) {
+        const int pc = __popc(__ballot_sync(kFull, (mism >> f) & 1u));
+        if (lane == f) c = pc;
+    }
+    if (c) atomicAdd(A.cnt + (t & 1) * A.G * 32 + g * 32 + lane, c);
+    if (__any_sync(kFull, c != 0) && lane == 0) atomicOr(A.any_bad + (t & 1), 1);
+}
+
+template <class Real, int D>
+constexpr int decode_min_blocks() { return (sizeof(Real) == 4 && D <= 16) ? 4 : 2; }
+
+constexpr int kDecodeThreads = 256;
+
+template <class Real, int D, bool DAMP, bool ISO>
+__global__ void __launch_bounds__(kDecodeThreads, decode_min_blocks<Real, D>())
+decode_kernel(const DecodeArgs<Real> A)
+{
+    const int lane = threadIdx.x & 31;
+    const int warps_per_block = blockDim.x >> 5;
+    const int gw = blockIdx.x * warps_per_block + (threadIdx.x >> 5);
+    const int nw = gridDim.x * warps_per_block;
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nthreads = gridDim.x * blockDim.x;
+    const int F = A.G * 32;
+    const int cblk = (A.C + 31) / 32;
+
+    // iteration 0: the uncorrected key against all u*m syndromes (_kernels.py:358-365)
+    for (int item = gw; item < A.G * cblk; item += nw)
+        syncheck_item<Real>(A, item / cblk, item % cblk, 0, kFull, lane);
+
+    int t = 1;
+    int final_t = 0;
+    for (;; ++t) {
+        grid_barrier(A.barrier);
+        const int* cprev = A.cnt + ((t - 1) & 1) * F;
+        // frames whose sweep t-1 decision satisfied every syndrome stop here
+        for (int f = gtid; f < F; f += nthreads) {
+            if (ld_cg(cprev + f) == 0 && A.iters[f] < 0) A.iters[f] = t - 1;
+            A.cnt[(t & 1) * F + f] = 0;
+        }
+        if (ld_cg(A.any_bad + ((t - 1) & 1)) == 0 || t > A.max_it) {
+            final_t = t - 1;
+            break;
+        }
+        if (gtid == 0) A.any_bad[t & 1] = 0;
+
+        for (int item = gw; item < A.G * A.C; item += nw) {
+            const int g = item / A.C;
+            const unsigned act = __ballot_sync(kFull, ld_cg(cprev + g * 32 + lane) != 0);
+            if (act) check_item<Real, D, DAMP, ISO>(A, g, item - g * A.C, t, act, lane);
+        }
+        grid_barrier(A.barrier);
+        for (int item = gw; item < A.G * A.n; item += nw) {
+            const int g = item / A.n;
+            const unsigned act = __ballot_sync(kFull, ld_cg(cprev + g * 32 + lane) != 0);
+            if (act) var_item<Real, ISO>(A, g, item - g * A.n, t, act, lane);
+        }
+        grid_barrier(A.barrier);
+        for (int item = gw; item < A.G * cblk; item += nw) {
+            const int g = item / cblk;
+            const unsigned act = __ballot_sync(kFull, ld_cg(cprev + g * 32 + lane) != 0);
+            if (act) syncheck_item<Real>(A, g, item - g * cblk, t, act, lane);
+        }
+    }
+
+    // per-frame results (DecodeResult fields, decoder.py:246-274)
+    const int* cfin = A.cnt + (final_t & 1) * F;
+    for (int f = gtid; f < A.B; f += nthreads) {
+        const int c = ld_cg(cfin + f);
+        int it = A.iters[f];
+        const bool conv = it >= 0;
+        A.out_conv[f] = conv ? 1 : 0;
+        A.out_iters[f] = conv ? it : A.max_it;
+        A.out_mism[f] = conv ? 0 : c;
+    }
+    if (gtid == 0) *A.sweeps_run = final_t;
+}
+
+// ---------------------------------------------------------------------------
+// bit-matrix transposes between BitBlock rows and 32-frame words
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned load_row_u32(const uint8_t* row, long long byte0, long long nbytes)
+{
+    unsigned x = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+        if (byte0 + b < nbytes) x |= (unsigned)row[byte0 + b] << (8 * b);
+    return x;
+}
+
+// 32x32 bit transpose across a warp: in lane l holds row l; out lane l holds
+// column l (bit f of out = bit l of lane f's input).
+__device__ __forceinline__ unsigned warp_transpose32(unsigned x, int lane)
+{
+    unsigned r = 0;
+#pragma unroll
+    for (int b = 0; b < 32; ++b) {
+        const unsigned w = __ballot_sync(kFull, (x >> b) & 1u);
+        if (lane == b) r = w;
+    }
+    return r;
+}
+
+// rows [B][row_bytes], bits [seg_off*8 + 32c, +32) of segment s of each row ->
+// words[g][word_off + 32c + lane].  grid-stride over (g, segment, chunk).
+__global__ void rows_to_words_kernel(const uint8_t* __restrict__ rows, long long row_bytes, int B,
+                                     int G, int nseg, int seg_bits, long long seg_bytes,
+                                     unsigned* __restrict__ words, unsigned* __restrict__ words2,
+                                     long long words_per_group)
+{
+    const int lane = threadIdx.x & 31;
+    const int chunks = (seg_bits + 31) / 32;
+    const long long total = (long long)G * nseg * chunks;
+    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long it = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < total; it += nw) {
+        const int c = (int)(it % chunks);
+        const int s = (int)((it / chunks) % nseg);
+        const int g = (int)(it / ((long long)chunks * nseg));
+        const int f = g * 32 + lane;
+        unsigned x = 0;
+        if (f < B) x = load_row_u32(rows + (long long)f * row_bytes + (long long)s * seg_bytes, 4LL * c, seg_bytes);
+        const unsigned w = warp_transpose32(x, lane);
+        const int bit = 32 * c + lane;
+        if (bit < seg_bits) {
+            const long long o = (long long)g * words_per_group + (long long)s * seg_bits + bit;
+            words[o] = w;
+            if (words2) words2[o] = w;
+        }
+    }
+}
+
+// words[g][word_off + 32c + lane] -> rows (inverse of rows_to_words_kernel)
+__global__ void words_to_rows_kernel(const unsigned* __restrict__ words, long long words_per_group,
+                                     int B, int G, int nseg, int seg_bits, long long seg_bytes,
+                                     uint8_t* __restrict__ rows, long long row_bytes)
+{
+    const int lane = threadIdx.x & 31;
+    const int chunks = (seg_bits + 31) / 32;
+    const long long total = (long long)G * nseg * chunks;
+    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long it = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < total; it += nw) {
+        const int c = (int)(it % chunks);
+        const int s = (int)((it / chunks) % nseg);
+        const int g = (int)(it / ((long long)chunks * nseg));
+        const int bit = 32 * c + lane;
+        const unsigned w = bit < seg_bits ? words[(long long)g * words_per_group + (long long)s * seg_bits + bit] : 0u;
+        const unsigned x = warp_transpose32(w, lane);
+        const int f = g * 32 + lane;
+        if (f < B) {
+            uint8_t* r = rows + (long long)f * row_bytes + (long long)s * seg_bytes;
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                if (4LL * c + b < seg_bytes) r[4LL * c + b] = (uint8_t)(x >> (8 * b));
+        }
+    }
+}
+
+// Alice side, Eq. 1: syndrome words of 32 frames per check, z = XOR of key
+// words over the row (syndrome_pass, _kernels.py:220-227, 32 frames wide).
+__global__ void syndrome_words_kernel(const int* __restrict__ chk_ptr, const int* __restrict__ chk_var,
+                                      int n, int C, int G, const unsigned* __restrict__ key_w,
+                                      unsigned* __restrict__ syn_w)
+{
+    const long long total = (long long)G * C;
+    const long long nth = (long long)gridDim.x * blockDim.x;
+    for (long long it = (long long)blockIdx.x * blockDim.x + threadIdx.x; it < total; it += nth) {
+        const int g = (int)(it / C), j = (int)(it % C);
+        const unsigned* kw = key_w + (long long)g * n;
+        unsigned p = 0;
+        for (int a = __ldg(chk_ptr + j); a < __ldg(chk_ptr + j + 1); ++a) p ^= __ldg(kw + __ldg(chk_var + a));
+        syn_w[it] = p;
+    }
+}
+
+// prior magnitude ln((1-e)/e) per frame (init_priors, decoder.py:147-152),
+// computed in double and stored in the message type; padding frames get 0.
+template <class Real>
+__global__ void prior_kernel(const double* __restrict__ e, int e_stride, int B, int F, Real* __restrict__ L)
+{
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f < F) {
+        double v = 0.0;
+        if (f < B) {
+            const double ef = e[(long long)f * e_stride];
+            v = log((1.0 - ef) / ef);
+        }
+        L[f] = (Real)v;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// single-frame phases on explicit messages (c2v_update / v2c_update /
+// soft_decision, decoder.py:155-200) -- thread per check / variable.
+// ---------------------------------------------------------------------------
+template <class Real, int D>
+__global__ void c2v_phase_kernel(const int* __restrict__ chk_ptr, int lo, int hi,
+                                 const uint8_t* __restrict__ syn_bits, Real clamp, float sat,
+                                 const Real* __restrict__ v2c, Real* __restrict__ c2v)
+{
+    const int j = lo + blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= hi) return;
+    const int e0 = chk_ptr[j], d = chk_ptr[j + 1] - e0;
+    Real x[D], out[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) x[k] = k < d ? v2c[e0 + k] : Real(0);
+    c2v_rule<D>(x, d, syn_bits[j - lo] ? 1u : 0u, clamp, sat, out);
+#pragma unroll
+    for (int k = 0; k < D; ++k)
+        if (k < d) c2v[e0 + k] = out[k];
+}
+
+template <class Real>
+__global__ void v2c_phase_kernel(const int* __restrict__ var_ptr, const int* __restrict__ var_edge,
+                                 int n, int lo_edge, int hi_edge, int joint, Real damping, Real clamp,
+                                 const Real* __restrict__ c2v, const Real* __restrict__ priors,
+                                 Real* __restrict__ v2c)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Real total = priors[i];
+    for (int t = var_ptr[i]; t < var_ptr[i + 1]; ++t) {
+        const int e = var_edge[t];
+        if (joint || (e >= lo_edge && e < hi_edge)) total += c2v[e];
+    }
+    for (int t = var_ptr[i]; t < var_ptr[i + 1]; ++t) {
+        const int e = var_edge[t];
+        if (e < lo_edge || e >= hi_edge) continue;
+        Real val = total - c2v[e];
+        if (damping != Real(0)) val = (Real(1) - damping) * val + damping * v2c[e];
+        v2c[e] = clampr(val, clamp);
+    }
+}
+
+template <class Real>
+__global__ void posterior_phase_kernel(const int* __restrict__ var_ptr, const int* __restrict__ var_edge,
+                                       int n, const Real* __restrict__ c2v,
+                                       const Real* __restrict__ priors, Real* __restrict__ post)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Real total = priors[i];
+    for (int t = var_ptr[i]; t < var_ptr[i + 1]; ++t) total += c2v[var_edge[t]];
+    post[i] = total;
+}
+
+// state readback: one frame's lane of an interleaved [..][32] array -> double
+template <class Real>
+__global__ void gather_lane_kernel(const Real* __restrict__ src, long long count, int lane,
+                                   double* __restrict__ dst)
+{
+    const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < count) dst[k] = (double)src[k * 32 + lane];
+}
+
+}  // namespace mbp

@@ -1,0 +1,765 @@
+// mbp.cu -- host side of libmbp_b200.so: the C ABI of include/mbp.h.
+//
+// Owns device copies of the stacked graph (mbp_ensemble) and per-batch
+// device buffers (mbp_workspace); enqueues the transposes and the persistent
+// cooperative decode kernel of kernels.cuh.  No torch, no Python: callers
+// bind it with ctypes (paper_2001_07979_b200/_native.py) or any FFI.
+#include "../../include/mbp.h"
+#include "kernels.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg)
+{
+    g_last_error = msg;
+    return code;
+}
+
+#define MBP_CUDA(call)                                                                          \
+    do {                                                                                        \
+        cudaError_t err__ = (call);                                                             \
+        if (err__ != cudaSuccess)                                                               \
+            return fail(MBP_ECUDA, std::string(#call) + ": " + cudaGetErrorString(err__));      \
+    } while (0)
+
+// Smallest double x with tanh(x/2) == 1.0 under the host libm -- where the
+// reference's float64 product saturates (_kernels.py:242, 249-252) -- rounded
+// up to float (the fp32 path compares float messages against it).
+float saturation_threshold()
+{
+    double lo = 1.0, hi = 100.0;
+    for (int k = 0; k < 200; ++k) {
+        const double mid = 0.5 * (lo + hi);
+        if (std::tanh(0.5 * mid) == 1.0) hi = mid; else lo = mid;
+    }
+    float f = (float)hi;
+    if ((double)f < hi) f = std::nextafter(f, INFINITY);
+    return f;
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~DevBuf() { if (p) cudaFree(p); }
+    int alloc(size_t b)
+    {
+        if (p) { cudaFree(p); p = nullptr; }
+        bytes = b;
+        if (!b) return MBP_OK;
+        if (cudaMalloc(&p, b) != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+            return fail(MBP_ENOMEM, "cudaMalloc of " + std::to_string(b) + " bytes failed");
+        }
+        return MBP_OK;
+    }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) { cudaGetDevice(&prev); if (prev != dev) cudaSetDevice(dev); }
+    ~DeviceGuard() { int cur; cudaGetDevice(&cur); if (prev >= 0 && cur != prev) cudaSetDevice(prev); }
+};
+
+int pick_degree(int dmax)
+{
+    if (dmax <= 8) return 8;
+    if (dmax <= 16) return 16;
+    if (dmax <= 32) return 32;
+    if (dmax <= 64) return 64;
+    return 0;
+}
+
+}  // namespace
+
+struct mbp_ensemble {
+    int n = 0, m = 0, u = 0, C = 0;
+    long long E = 0;
+    int dmax_c = 0, dmax_v = 0;
+    int device = 0, sm_count = 0;
+    float sat = 0.f;
+    std::vector<long long> edge_off;  // [u+1]
+    DevBuf chk_ptr, chk_var, var_ptr, var_edge;  // int32
+};
+
+struct mbp_workspace {
+    mbp_ensemble* ens = nullptr;
+    mbp_decoder_config cfg{};
+    int cap = 0, G = 0;
+    size_t real_size = 4;
+    DevBuf c2v, post, v2c, Lmag, noisy_w, syn_w, hard_w, hist_w, cnt, any_bad, iters, barrier,
+        sweeps, tmp_in, tmp_out, tmp_conv, tmp_iters, tmp_mism, tmp_e;
+    cudaStream_t own_stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+    int last_B = 0;
+    bool timed = false, e2e_timed = false;
+    ~mbp_workspace()
+    {
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (ev2) cudaEventDestroy(ev2);
+        if (ev3) cudaEventDestroy(ev3);
+        if (own_stream) cudaStreamDestroy(own_stream);
+    }
+};
+
+// Exported functions take C linkage from their declarations in mbp.h.
+
+const char* mbp_last_error(void) { return g_last_error.c_str(); }
+
+const char* mbp_version(void) { return "mbp_b200 0.1.0 (sm_100a)"; }
+
+int mbp_device_count(int* count)
+{
+    if (!count) return fail(MBP_EINVAL, "count is null");
+    MBP_CUDA(cudaGetDeviceCount(count));
+    return MBP_OK;
+}
+
+int mbp_ensemble_create(int32_t n, int32_t m, int32_t u, const int64_t* chk_ptr,
+                        const int32_t* chk_var, int device, mbp_ensemble** out)
+{
+    if (!out || !chk_ptr || !chk_var) return fail(MBP_EINVAL, "null pointer argument");
+    *out = nullptr;
+    if (!(0 < m && 0 < n)) return fail(MBP_EINVAL, "need m > 0 and n > 0, got m=" + std::to_string(m) + ", n=" + std::to_string(n));
+    if (u < 1 || u > MBP_MAX_MATRICES) return fail(MBP_EINVAL, "u must be in [1, " + std::to_string(MBP_MAX_MATRICES) + "]");
+    const long long C = (long long)u * m;
+    const long long E = chk_ptr[C];
+    if (chk_ptr[0] != 0 || E <= 0 || E >= (1LL << 31) / 32)
+        return fail(MBP_EINVAL, "bad stacked chk_ptr (edge count " + std::to_string(E) + ")");
+    auto* ens = new mbp_ensemble;
+    ens->n = n; ens->m = m; ens->u = u; ens->C = (int)C; ens->E = E; ens->device = device;
+    std::vector<int> cp(C + 1), cv(E), col_deg(n, 0);
+    int dmax_c = 0;
+    for (long long j = 0; j < C; ++j) {
+        if (chk_ptr[j + 1] < chk_ptr[j]) { delete ens; return fail(MBP_EINVAL, "chk_ptr not monotone"); }
+        dmax_c = std::max<int>(dmax_c, (int)(chk_ptr[j + 1] - chk_ptr[j]));
+        cp[j] = (int)chk_ptr[j];
+    }
+    cp[C] = (int)E;
+    for (long long e = 0; e < E; ++e) {
+        const int v = chk_var[e];
+        if (v < 0 || v >= n) { delete ens; return fail(MBP_EINVAL, "variable index out of range at edge " + std::to_string(e)); }
+        cv[e] = v;
+        ++col_deg[v];
+    }
+    // edge_off: matrix l owns edges [chk_ptr[l*m], chk_ptr[(l+1)*m])
+    ens->edge_off.resize(u + 1);
+    for (int l = 0; l <= u; ++l) ens->edge_off[l] = chk_ptr[(long long)l * m];
+    // variable side: stable counting sort of edges by variable (ascending ids)
+    std::vector<int> vp(n + 1, 0), ve(E);
+    int dmax_v = 0;
+    for (int i = 0; i < n; ++i) {
+        if (col_deg[i] == 0) { delete ens; return fail(MBP_EINVAL, "variable " + std::to_string(i) + " has degree 0"); }
+        vp[i + 1] = vp[i] + col_deg[i];
+        dmax_v = std::max(dmax_v, col_deg[i]);
+    }
+    {
+        std::vector<int> fill(vp.begin(), vp.end() - 1);
+        for (long long e = 0; e < E; ++e) ve[fill[cv[e]]++] = (int)e;
+    }
+    ens->dmax_c = dmax_c;
+    ens->dmax_v = dmax_v;
+    ens->sat = saturation_threshold();
+    int rc;
+    {
+        DeviceGuard dg(device);
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
+            delete ens;
+            cudaGetLastError();
+            return fail(MBP_ECUDA, "no CUDA device " + std::to_string(device));
+        }
+        ens->sm_count = prop.multiProcessorCount;
+        if ((rc = ens->chk_ptr.alloc(sizeof(int) * (C + 1))) || (rc = ens->chk_var.alloc(sizeof(int) * E)) ||
+            (rc = ens->var_ptr.alloc(sizeof(int) * (n + 1))) || (rc = ens->var_edge.alloc(sizeof(int) * E))) {
+            delete ens;
+            return rc;
+        }
+        cudaError_t err = cudaMemcpy(ens->chk_ptr.p, cp.data(), sizeof(int) * (C + 1), cudaMemcpyHostToDevice);
+        if (err == cudaSuccess) err = cudaMemcpy(ens->chk_var.p, cv.data(), sizeof(int) * E, cudaMemcpyHostToDevice);
+        if (err == cudaSuccess) err = cudaMemcpy(ens->var_ptr.p, vp.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice);
+        if (err == cudaSuccess) err = cudaMemcpy(ens->var_edge.p, ve.data(), sizeof(int) * E, cudaMemcpyHostToDevice);
+        if (err != cudaSuccess) { delete ens; return fail(MBP_ECUDA, std::string("ensemble upload: ") + cudaGetErrorString(err)); }
+    }
+    *out = ens;
+    return MBP_OK;
+}
+
+int mbp_ensemble_destroy(mbp_ensemble* ens)
+{
+    if (ens) { DeviceGuard dg(ens->device); delete ens; }
+    return MBP_OK;
+}
+
+int mbp_ensemble_get_info(const mbp_ensemble* ens, mbp_ensemble_info* info)
+{
+    if (!ens || !info) return fail(MBP_EINVAL, "null pointer argument");
+    info->n = ens->n; info->m = ens->m; info->u = ens->u; info->edges = ens->E;
+    info->max_check_degree = ens->dmax_c; info->max_var_degree = ens->dmax_v;
+    info->device = ens->device; info->sm_count = ens->sm_count;
+    return MBP_OK;
+}
+
+static int validate_cfg(const mbp_decoder_config* cfg)
+{
+    if (!cfg) return fail(MBP_EINVAL, "config is null");
+    if (cfg->max_iterations < 1) return fail(MBP_EINVAL, "max_iterations must be >= 1, got " + std::to_string(cfg->max_iterations));
+    if (!(cfg->llr_clamp > 0)) return fail(MBP_EINVAL, "llr_clamp must be positive");
+    if (!(cfg->damping >= 0.0 && cfg->damping <= 1.0)) return fail(MBP_EINVAL, "damping must be in [0, 1]");
+    if (cfg->combining_mode != MBP_JOINT_GRAPH && cfg->combining_mode != MBP_ISOLATED_PER_MATRIX)
+        return fail(MBP_EINVAL, "combining_mode must be joint-graph or isolated-per-matrix");
+    if (cfg->precision != MBP_FP32_PHI && cfg->precision != MBP_FP64_TANH)
+        return fail(MBP_EINVAL, "precision must be MBP_FP32_PHI or MBP_FP64_TANH");
+    return MBP_OK;
+}
+
+// (Re)allocate the buffers whose shape depends on cfg.
+static int ws_alloc(mbp_workspace* ws)
+{
+    const mbp_ensemble* ens = ws->ens;
+    const size_t F = (size_t)ws->G * 32, R = ws->real_size;
+    const size_t P = ws->cfg.combining_mode == MBP_ISOLATED_PER_MATRIX ? (size_t)ens->u + 1 : 1;
+    int rc;
+    if (ws->c2v.bytes != ws->G * (size_t)ens->E * 32 * R && (rc = ws->c2v.alloc(ws->G * (size_t)ens->E * 32 * R))) return rc;
+    if (ws->post.bytes != ws->G * P * ens->n * 32 * R && (rc = ws->post.alloc(ws->G * P * ens->n * 32 * R))) return rc;
+    const size_t v2c_bytes = ws->cfg.damping != 0.0 ? ws->G * (size_t)ens->E * 32 * R : 0;
+    if (ws->v2c.bytes != v2c_bytes && (rc = ws->v2c.alloc(v2c_bytes))) return rc;
+    const size_t hist_bytes = (ws->cfg.flags & MBP_RECORD_HISTORY)
+        ? (size_t)(ws->cfg.max_iterations + 1) * ws->G * ens->n * 4 : 0;
+    if (ws->hist_w.bytes != hist_bytes && (rc = ws->hist_w.alloc(hist_bytes))) return rc;
+    if (!ws->Lmag.p) {
+        if ((rc = ws->Lmag.alloc(F * R)) || (rc = ws->noisy_w.alloc((size_t)ws->G * ens->n * 4)) ||
+            (rc = ws->syn_w.alloc((size_t)ws->G * ens->C * 4)) || (rc = ws->hard_w.alloc((size_t)ws->G * ens->n * 4)) ||
+            (rc = ws->cnt.alloc(2 * F * 4)) || (rc = ws->any_bad.alloc(2 * 4)) || (rc = ws->iters.alloc(F * 4)) ||
+            (rc = ws->barrier.alloc(2 * 4)) || (rc = ws->sweeps.alloc(4)))
+            return rc;
+    }
+    return MBP_OK;
+}
+
+int mbp_workspace_create(mbp_ensemble* ens, int32_t max_frames, const mbp_decoder_config* cfg,
+                         mbp_workspace** out)
+{
+    if (!ens || !out) return fail(MBP_EINVAL, "null pointer argument");
+    *out = nullptr;
+    int rc = validate_cfg(cfg);
+    if (rc) return rc;
+    if (max_frames < 1) return fail(MBP_EINVAL, "max_frames must be >= 1");
+    if (!pick_degree(ens->dmax_c))
+        return fail(MBP_EUNSUPPORTED, "check degree " + std::to_string(ens->dmax_c) + " exceeds MBP_MAX_CHECK_DEGREE");
+    DeviceGuard dg(ens->device);
+    auto* ws = new mbp_workspace;
+    ws->ens = ens;
+    ws->cfg = *cfg;
+    ws->cap = max_frames;
+    ws->G = (max_frames + 31) / 32;
+    ws->real_size = cfg->precision == MBP_FP64_TANH ? 8 : 4;
+    if ((rc = ws_alloc(ws))) { delete ws; return rc; }
+    if (cudaStreamCreateWithFlags(&ws->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreate(&ws->ev0) != cudaSuccess || cudaEventCreate(&ws->ev1) != cudaSuccess ||
+        cudaEventCreate(&ws->ev2) != cudaSuccess || cudaEventCreate(&ws->ev3) != cudaSuccess) {
+        delete ws;
+        cudaGetLastError();
+        return fail(MBP_ECUDA, "stream/event creation failed");
+    }
+    *out = ws;
+    return MBP_OK;
+}
+
+int mbp_workspace_destroy(mbp_workspace* ws)
+{
+    if (ws) { DeviceGuard dg(ws->ens->device); delete ws; }
+    return MBP_OK;
+}
+
+int mbp_workspace_configure(mbp_workspace* ws, const mbp_decoder_config* cfg)
+{
+    if (!ws) return fail(MBP_EINVAL, "workspace is null");
+    int rc = validate_cfg(cfg);
+    if (rc) return rc;
+    if (cfg->precision != ws->cfg.precision || cfg->combining_mode != ws->cfg.combining_mode)
+        return fail(MBP_EINVAL, "precision and combining_mode are fixed at workspace creation");
+    DeviceGuard dg(ws->ens->device);
+    ws->cfg = *cfg;
+    return ws_alloc(ws);
+}
+
+// ---------------------------------------------------------------------------
+// launch helpers
+// ---------------------------------------------------------------------------
+static int grid_for(long long warps_needed)
+{
+    long long blocks = (warps_needed + 7) / 8;
+    return (int)std::max(1LL, std::min(blocks, 148LL * 16));
+}
+
+static int launch_rows_to_words(const uint8_t* rows, long long row_bytes, int B, int G, int nseg,
+                                int seg_bits, long long seg_bytes, unsigned* words, unsigned* words2,
+                                long long wpg, cudaStream_t s)
+{
+    const long long items = (long long)G * nseg * ((seg_bits + 31) / 32);
+    mbp::rows_to_words_kernel<<<grid_for(items), 256, 0, s>>>(rows, row_bytes, B, G, nseg, seg_bits,
+                                                               seg_bytes, words, words2, wpg);
+    MBP_CUDA(cudaGetLastError());
+    return MBP_OK;
+}
+
+static int launch_words_to_rows(const unsigned* words, long long wpg, int B, int G, int nseg,
+                                int seg_bits, long long seg_bytes, uint8_t* rows, long long row_bytes,
+                                cudaStream_t s)
+{
+    const long long items = (long long)G * nseg * ((seg_bits + 31) / 32);
+    mbp::words_to_rows_kernel<<<grid_for(items), 256, 0, s>>>(words, wpg, B, G, nseg, seg_bits, seg_bytes,
+                                                              rows, row_bytes);
+    MBP_CUDA(cudaGetLastError());
+    return MBP_OK;
+}
+
+template <class Real, int D, bool DAMP, bool ISO>
+static int launch_decode(mbp_workspace* ws, mbp::DecodeArgs<Real>& A, cudaStream_t s)
+{
+    auto kern = mbp::decode_kernel<Real, D, DAMP, ISO>;
+    int per_sm = 0;
+    MBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, mbp::kDecodeThreads, 0));
+    if (per_sm < 1) return fail(MBP_ECUDA, "decode kernel cannot be resident");
+    const int grid = per_sm * ws->ens->sm_count;
+    void* args[] = {(void*)&A};
+    MBP_CUDA(cudaEventRecord(ws->ev0, s));
+    MBP_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(mbp::kDecodeThreads), args, 0, s));
+    MBP_CUDA(cudaEventRecord(ws->ev1, s));
+    ws->timed = true;
+    return MBP_OK;
+}
+
+template <class Real>
+static int dispatch_decode(mbp_workspace* ws, mbp::DecodeArgs<Real>& A, cudaStream_t s)
+{
+    const bool damp = ws->cfg.damping != 0.0;
+    const bool iso = ws->cfg.combining_mode == MBP_ISOLATED_PER_MATRIX;
+#define MBP_DISPATCH_D(D)                                                            \
+    if (damp && iso) return launch_decode<Real, D, true, true>(ws, A, s);            \
+    if (damp) return launch_decode<Real, D, true, false>(ws, A, s);                  \
+    if (iso) return launch_decode<Real, D, false, true>(ws, A, s);                   \
+    return launch_decode<Real, D, false, false>(ws, A, s);
+    switch (pick_degree(ws->ens->dmax_c)) {
+    case 8: { MBP_DISPATCH_D(8) }
+    case 16: { MBP_DISPATCH_D(16) }
+    case 32: { MBP_DISPATCH_D(32) }
+    case 64: { MBP_DISPATCH_D(64) }
+    default: return fail(MBP_EUNSUPPORTED, "check degree too large");
+    }
+#undef MBP_DISPATCH_D
+}
+
+template <class Real>
+static __global__ void fill_post_prior_kernel(const unsigned* __restrict__ noisy_w, const Real* __restrict__ L,
+                                              int G, int n, int P, Real* __restrict__ post)
+{
+    const long long total = (long long)G * P * n * 32;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < total;
+         k += (long long)gridDim.x * blockDim.x) {
+        const int lane = (int)(k & 31);
+        const int i = (int)((k >> 5) % n);
+        const int g = (int)((k >> 5) / ((long long)n * P));
+        const unsigned w = noisy_w[(long long)g * n + i];
+        const Real l = L[g * 32 + lane];
+        post[k] = ((w >> lane) & 1u) ? -l : l;
+    }
+}
+
+template <class Real>
+static int decode_chunk(mbp_workspace* ws, const uint8_t* noisy, const uint8_t* syn, const double* e,
+                        int e_stride, int B, uint8_t* corrected, uint8_t* conv, int* iters, int* mism,
+                        cudaStream_t s)
+{
+    const mbp_ensemble* ens = ws->ens;
+    const int G = (B + 31) / 32, F = G * 32;
+    const long long nb = (ens->n + 7) / 8, mb = (ens->m + 7) / 8;
+    const mbp_decoder_config& cfg = ws->cfg;
+    int rc;
+    mbp::prior_kernel<Real><<<(F + 255) / 256, 256, 0, s>>>(e, e_stride, B, F, ws->Lmag.as<Real>());
+    MBP_CUDA(cudaGetLastError());
+    if ((rc = launch_rows_to_words(noisy, nb, B, G, 1, ens->n, nb, ws->noisy_w.as<unsigned>(),
+                                   ws->hard_w.as<unsigned>(), ens->n, s)))
+        return rc;
+    if ((rc = launch_rows_to_words(syn, (long long)ens->u * mb, B, G, ens->u, ens->m, mb,
+                                   ws->syn_w.as<unsigned>(), nullptr, ens->C, s)))
+        return rc;
+    const bool record = (cfg.flags & MBP_RECORD_HISTORY) != 0;
+    if (record)
+        MBP_CUDA(cudaMemcpyAsync(ws->hist_w.p, ws->noisy_w.p, (size_t)G * ens->n * 4, cudaMemcpyDeviceToDevice, s));
+    if (cfg.flags & MBP_KEEP_STATE) {
+        const int P = cfg.combining_mode == MBP_ISOLATED_PER_MATRIX ? ens->u + 1 : 1;
+        fill_post_prior_kernel<Real><<<1024, 256, 0, s>>>(ws->noisy_w.as<unsigned>(), ws->Lmag.as<Real>(), G,
+                                                          ens->n, P, ws->post.as<Real>());
+        MBP_CUDA(cudaGetLastError());
+        MBP_CUDA(cudaMemsetAsync(ws->c2v.p, 0, (size_t)G * ens->E * 32 * sizeof(Real), s));
+    }
+    MBP_CUDA(cudaMemsetAsync(ws->cnt.p, 0, 2 * (size_t)F * 4, s));
+    MBP_CUDA(cudaMemsetAsync(ws->any_bad.p, 0, 8, s));
+    MBP_CUDA(cudaMemsetAsync(ws->iters.p, 0xff, (size_t)F * 4, s));
+    MBP_CUDA(cudaMemsetAsync(ws->barrier.p, 0, 8, s));
+
+    mbp::DecodeArgs<Real> A;
+    std::memset(&A, 0, sizeof A);
+    A.n = ens->n; A.m = ens->m; A.u = ens->u; A.C = ens->C; A.E = (int)ens->E;
+    A.chk_ptr = ens->chk_ptr.as<int>(); A.chk_var = ens->chk_var.as<int>();
+    A.var_ptr = ens->var_ptr.as<int>(); A.var_edge = ens->var_edge.as<int>();
+    for (int l = 0; l <= ens->u; ++l) A.edge_off[l] = (int)ens->edge_off[l];
+    A.G = G;
+    A.c2v = ws->c2v.as<Real>(); A.post = ws->post.as<Real>(); A.v2c = ws->v2c.as<Real>();
+    A.Lmag = ws->Lmag.as<Real>();
+    A.noisy_w = ws->noisy_w.as<unsigned>(); A.syn_w = ws->syn_w.as<unsigned>();
+    A.hard_w = ws->hard_w.as<unsigned>(); A.hist_w = record ? ws->hist_w.as<unsigned>() : nullptr;
+    A.cnt = ws->cnt.as<int>(); A.any_bad = ws->any_bad.as<int>(); A.iters = ws->iters.as<int>();
+    A.barrier = ws->barrier.as<unsigned>(); A.sweeps_run = ws->sweeps.as<int>();
+    A.B = B; A.out_conv = conv; A.out_iters = iters; A.out_mism = mism;
+    A.max_it = cfg.max_iterations; A.clamp = (Real)cfg.llr_clamp; A.damping = (Real)cfg.damping;
+    A.sat = ens->sat;
+    if ((rc = dispatch_decode<Real>(ws, A, s))) return rc;
+    if ((rc = launch_words_to_rows(ws->hard_w.as<unsigned>(), ens->n, B, G, 1, ens->n, nb, corrected, nb, s)))
+        return rc;
+    ws->last_B = B;
+    return MBP_OK;
+}
+
+int mbp_decode_batch_device(mbp_workspace* ws, const uint8_t* noisy, const uint8_t* syn, const double* e,
+                            int32_t e_stride, int64_t batch, uint8_t* corrected, uint8_t* converged,
+                            int32_t* iterations, int32_t* mismatches, void* stream)
+{
+    if (!ws || !noisy || !syn || !e || !corrected || !converged || !iterations || !mismatches)
+        return fail(MBP_EINVAL, "null pointer argument");
+    if (batch < 0) return fail(MBP_EINVAL, "negative batch");
+    if (e_stride != 0 && e_stride != 1) return fail(MBP_EINVAL, "e_stride must be 0 or 1");
+    if (batch == 0) return MBP_OK;
+    const mbp_ensemble* ens = ws->ens;
+    DeviceGuard dg(ens->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const long long nb = (ens->n + 7) / 8, sb = (long long)ens->u * ((ens->m + 7) / 8);
+    for (int64_t off = 0; off < batch; off += ws->cap) {
+        const int B = (int)std::min<int64_t>(ws->cap, batch - off);
+        int rc = ws->real_size == 8
+            ? decode_chunk<double>(ws, noisy + off * nb, syn + off * sb, e + off * e_stride, e_stride, B,
+                                   corrected + off * nb, converged + off, iterations + off, mismatches + off, s)
+            : decode_chunk<float>(ws, noisy + off * nb, syn + off * sb, e + off * e_stride, e_stride, B,
+                                  corrected + off * nb, converged + off, iterations + off, mismatches + off, s);
+        if (rc) return rc;
+    }
+    return MBP_OK;
+}
+
+// host-buffer variant: stage through the workspace's device scratch
+static int ensure(DevBuf& b, size_t bytes)
+{
+    return b.bytes >= bytes ? MBP_OK : b.alloc(bytes);
+}
+
+int mbp_decode_batch(mbp_workspace* ws, const uint8_t* noisy, const uint8_t* syn, const double* e,
+                     int32_t e_stride, int64_t batch, uint8_t* corrected, uint8_t* converged,
+                     int32_t* iterations, int32_t* mismatches)
+{
+    if (!ws || !noisy || !syn || !e || !corrected || !converged || !iterations || !mismatches)
+        return fail(MBP_EINVAL, "null pointer argument");
+    if (e_stride != 0 && e_stride != 1) return fail(MBP_EINVAL, "e_stride must be 0 or 1");
+    if (batch <= 0) return batch == 0 ? MBP_OK : fail(MBP_EINVAL, "negative batch");
+    const mbp_ensemble* ens = ws->ens;
+    DeviceGuard dg(ens->device);
+    cudaStream_t s = ws->own_stream;
+    const size_t nb = (ens->n + 7) / 8, sb = (size_t)ens->u * ((ens->m + 7) / 8);
+    const size_t ne = e_stride ? (size_t)batch : 1;
+    int rc;
+    if ((rc = ensure(ws->tmp_in, batch * (nb + sb))) || (rc = ensure(ws->tmp_out, batch * nb)) ||
+        (rc = ensure(ws->tmp_conv, batch)) || (rc = ensure(ws->tmp_iters, batch * 4)) ||
+        (rc = ensure(ws->tmp_mism, batch * 4)) || (rc = ensure(ws->tmp_e, ne * 8)))
+        return rc;
+    uint8_t* d_noisy = ws->tmp_in.as<uint8_t>();
+    uint8_t* d_syn = d_noisy + batch * nb;
+    MBP_CUDA(cudaEventRecord(ws->ev2, s));
+    MBP_CUDA(cudaMemcpyAsync(d_noisy, noisy, batch * nb, cudaMemcpyHostToDevice, s));
+    MBP_CUDA(cudaMemcpyAsync(d_syn, syn, batch * sb, cudaMemcpyHostToDevice, s));
+    MBP_CUDA(cudaMemcpyAsync(ws->tmp_e.p, e, ne * 8, cudaMemcpyHostToDevice, s));
+    if ((rc = mbp_decode_batch_device(ws, d_noisy, d_syn, ws->tmp_e.as<double>(), e_stride, batch,
+                                      ws->tmp_out.as<uint8_t>(), ws->tmp_conv.as<uint8_t>(),
+                                      ws->tmp_iters.as<int>(), ws->tmp_mism.as<int>(), s)))
+        return rc;
+    MBP_CUDA(cudaMemcpyAsync(corrected, ws->tmp_out.p, batch * nb, cudaMemcpyDeviceToHost, s));
+    MBP_CUDA(cudaMemcpyAsync(converged, ws->tmp_conv.p, batch, cudaMemcpyDeviceToHost, s));
+    MBP_CUDA(cudaMemcpyAsync(iterations, ws->tmp_iters.p, batch * 4, cudaMemcpyDeviceToHost, s));
+    MBP_CUDA(cudaMemcpyAsync(mismatches, ws->tmp_mism.p, batch * 4, cudaMemcpyDeviceToHost, s));
+    MBP_CUDA(cudaEventRecord(ws->ev3, s));
+    MBP_CUDA(cudaStreamSynchronize(s));
+    ws->e2e_timed = true;
+    return MBP_OK;
+}
+
+int mbp_syndrome_batch_device(mbp_workspace* ws, const uint8_t* keys, int64_t batch, uint8_t* syn, void* stream)
+{
+    if (!ws || !keys || !syn) return fail(MBP_EINVAL, "null pointer argument");
+    if (batch < 0) return fail(MBP_EINVAL, "negative batch");
+    const mbp_ensemble* ens = ws->ens;
+    DeviceGuard dg(ens->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const long long nb = (ens->n + 7) / 8, mb = (ens->m + 7) / 8, sb = (long long)ens->u * mb;
+    for (int64_t off = 0; off < batch; off += ws->cap) {
+        const int B = (int)std::min<int64_t>(ws->cap, batch - off);
+        const int G = (B + 31) / 32;
+        int rc;
+        if ((rc = launch_rows_to_words(keys + off * nb, nb, B, G, 1, ens->n, nb, ws->noisy_w.as<unsigned>(),
+                                       nullptr, ens->n, s)))
+            return rc;
+        const long long items = (long long)G * ens->C;
+        mbp::syndrome_words_kernel<<<(int)std::min<long long>((items + 255) / 256, 148LL * 32), 256, 0, s>>>(
+            ens->chk_ptr.as<int>(), ens->chk_var.as<int>(), ens->n, ens->C, G, ws->noisy_w.as<unsigned>(),
+            ws->syn_w.as<unsigned>());
+        MBP_CUDA(cudaGetLastError());
+        if ((rc = launch_words_to_rows(ws->syn_w.as<unsigned>(), ens->C, B, G, ens->u, ens->m, mb,
+                                       syn + off * sb, sb, s)))
+            return rc;
+    }
+    return MBP_OK;
+}
+
+int mbp_syndrome_batch(mbp_workspace* ws, const uint8_t* keys, int64_t batch, uint8_t* syn)
+{
+    if (!ws || !keys || !syn) return fail(MBP_EINVAL, "null pointer argument");
+    if (batch <= 0) return batch == 0 ? MBP_OK : fail(MBP_EINVAL, "negative batch");
+    const mbp_ensemble* ens = ws->ens;
+    DeviceGuard dg(ens->device);
+    cudaStream_t s = ws->own_stream;
+    const size_t nb = (ens->n + 7) / 8, sb = (size_t)ens->u * ((ens->m + 7) / 8);
+    int rc;
+    if ((rc = ensure(ws->tmp_in, batch * nb)) || (rc = ensure(ws->tmp_out, batch * sb))) return rc;
+    MBP_CUDA(cudaMemcpyAsync(ws->tmp_in.p, keys, batch * nb, cudaMemcpyHostToDevice, s));
+    if ((rc = mbp_syndrome_batch_device(ws, ws->tmp_in.as<uint8_t>(), batch, ws->tmp_out.as<uint8_t>(), s)))
+        return rc;
+    MBP_CUDA(cudaMemcpyAsync(syn, ws->tmp_out.p, batch * sb, cudaMemcpyDeviceToHost, s));
+    MBP_CUDA(cudaStreamSynchronize(s));
+    return MBP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// state readback
+// ---------------------------------------------------------------------------
+static int read_lane(mbp_workspace* ws, const void* base, long long count, int64_t frame, double* out)
+{
+    DevBuf tmp;
+    int rc;
+    if ((rc = tmp.alloc(count * 8))) return rc;
+    const int lane = (int)(frame & 31);
+    if (ws->real_size == 8)
+        mbp::gather_lane_kernel<double><<<(int)((count + 255) / 256), 256>>>((const double*)base, count, lane, tmp.as<double>());
+    else
+        mbp::gather_lane_kernel<float><<<(int)((count + 255) / 256), 256>>>((const float*)base, count, lane, tmp.as<double>());
+    MBP_CUDA(cudaGetLastError());
+    MBP_CUDA(cudaMemcpy(out, tmp.p, count * 8, cudaMemcpyDeviceToHost));
+    return MBP_OK;
+}
+
+int mbp_workspace_read_posterior(mbp_workspace* ws, int64_t frame, double* posterior)
+{
+    if (!ws || !posterior) return fail(MBP_EINVAL, "null pointer argument");
+    if (!(ws->cfg.flags & MBP_KEEP_STATE)) return fail(MBP_EINVAL, "workspace was not configured with MBP_KEEP_STATE");
+    if (frame < 0 || frame >= ws->last_B) return fail(MBP_EINVAL, "frame outside the last batch");
+    const mbp_ensemble* ens = ws->ens;
+    DeviceGuard dg(ens->device);
+    MBP_CUDA(cudaStreamSynchronize(ws->own_stream));
+    MBP_CUDA(cudaDeviceSynchronize());
+    const size_t P = ws->cfg.combining_mode == MBP_ISOLATED_PER_MATRIX ? (size_t)ens->u + 1 : 1;
+    const size_t g = frame / 32;
+    const char* base = ws->post.as<char>() + ((g * P + (P - 1)) * ens->n * 32) * ws->real_size;
+    return read_lane(ws, base, ens->n, frame, posterior);
+}
+
+int mbp_workspace_read_c2v(mbp_workspace* ws, int64_t frame, double* c2v)
+{
+    if (!ws || !c2v) return fail(MBP_EINVAL, "null pointer argument");
+    if (!(ws->cfg.flags & MBP_KEEP_STATE)) return fail(MBP_EINVAL, "workspace was not configured with MBP_KEEP_STATE");
+    if (frame < 0 || frame >= ws->last_B) return fail(MBP_EINVAL, "frame outside the last batch");
+    const mbp_ensemble* ens = ws->ens;
+    DeviceGuard dg(ens->device);
+    MBP_CUDA(cudaDeviceSynchronize());
+    const char* base = ws->c2v.as<char>() + ((size_t)(frame / 32) * ens->E * 32) * ws->real_size;
+    return read_lane(ws, base, ens->E, frame, c2v);
+}
+
+int mbp_workspace_read_v2c(mbp_workspace* ws, int64_t frame, double* v2c)
+{
+    if (!ws || !v2c) return fail(MBP_EINVAL, "null pointer argument");
+    if (!ws->v2c.p) return fail(MBP_EINVAL, "workspace keeps no v2c buffer (damping == 0)");
+    if (frame < 0 || frame >= ws->last_B) return fail(MBP_EINVAL, "frame outside the last batch");
+    const mbp_ensemble* ens = ws->ens;
+    DeviceGuard dg(ens->device);
+    MBP_CUDA(cudaDeviceSynchronize());
+    const char* base = ws->v2c.as<char>() + ((size_t)(frame / 32) * ens->E * 32) * ws->real_size;
+    return read_lane(ws, base, ens->E, frame, v2c);
+}
+
+int mbp_workspace_read_history(mbp_workspace* ws, int64_t frame, int32_t rows, uint8_t* out)
+{
+    if (!ws || !out) return fail(MBP_EINVAL, "null pointer argument");
+    if (!(ws->cfg.flags & MBP_RECORD_HISTORY)) return fail(MBP_EINVAL, "workspace was not configured with MBP_RECORD_HISTORY");
+    if (frame < 0 || frame >= ws->last_B) return fail(MBP_EINVAL, "frame outside the last batch");
+    if (rows < 0 || rows > ws->cfg.max_iterations + 1) return fail(MBP_EINVAL, "rows out of range");
+    const mbp_ensemble* ens = ws->ens;
+    DeviceGuard dg(ens->device);
+    MBP_CUDA(cudaDeviceSynchronize());
+    const size_t n = ens->n, nb = (n + 7) / 8, g = frame / 32;
+    const int lane = (int)(frame & 31);
+    std::vector<unsigned> w(n);
+    for (int t = 0; t < rows; ++t) {
+        MBP_CUDA(cudaMemcpy(w.data(), ws->hist_w.as<unsigned>() + ((size_t)t * ws->G + g) * n, n * 4,
+                            cudaMemcpyDeviceToHost));
+        uint8_t* r = out + t * nb;
+        std::memset(r, 0, nb);
+        for (size_t i = 0; i < n; ++i) r[i >> 3] |= (uint8_t)(((w[i] >> lane) & 1u) << (i & 7));
+    }
+    return MBP_OK;
+}
+
+int mbp_workspace_last_timing(mbp_workspace* ws, float* ms, float* e2e_ms, int32_t* sweeps)
+{
+    if (!ws) return fail(MBP_EINVAL, "workspace is null");
+    DeviceGuard dg(ws->ens->device);
+    if (ms) {
+        if (!ws->timed) return fail(MBP_EINVAL, "no decode has run");
+        MBP_CUDA(cudaEventSynchronize(ws->ev1));
+        MBP_CUDA(cudaEventElapsedTime(ms, ws->ev0, ws->ev1));
+    }
+    if (e2e_ms) {
+        if (!ws->e2e_timed) return fail(MBP_EINVAL, "no host-buffer decode has run");
+        MBP_CUDA(cudaEventSynchronize(ws->ev3));
+        MBP_CUDA(cudaEventElapsedTime(e2e_ms, ws->ev2, ws->ev3));
+    }
+    if (sweeps) MBP_CUDA(cudaMemcpy(sweeps, ws->sweeps.p, 4, cudaMemcpyDeviceToHost));
+    return MBP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// single phases (c2v_update / v2c_update / soft_decision)
+// ---------------------------------------------------------------------------
+template <class Real>
+static int phase_c2v(mbp_ensemble* ens, int l, const uint8_t* syn_bits, double clamp, const double* v2c, double* c2v)
+{
+    const size_t E = ens->E;
+    std::vector<Real> hv(E), hc(E);
+    for (size_t k = 0; k < E; ++k) { hv[k] = (Real)v2c[k]; hc[k] = (Real)c2v[k]; }
+    DevBuf dv, dc, ds;
+    int rc;
+    if ((rc = dv.alloc(E * sizeof(Real))) || (rc = dc.alloc(E * sizeof(Real))) || (rc = ds.alloc(ens->m))) return rc;
+    MBP_CUDA(cudaMemcpy(dv.p, hv.data(), E * sizeof(Real), cudaMemcpyHostToDevice));
+    MBP_CUDA(cudaMemcpy(dc.p, hc.data(), E * sizeof(Real), cudaMemcpyHostToDevice));
+    MBP_CUDA(cudaMemcpy(ds.p, syn_bits, ens->m, cudaMemcpyHostToDevice));
+    const int lo = l * ens->m, hi = lo + ens->m, grid = (ens->m + 127) / 128;
+#define MBP_C2V(D) mbp::c2v_phase_kernel<Real, D><<<grid, 128>>>(ens->chk_ptr.as<int>(), lo, hi, ds.as<uint8_t>(), (Real)clamp, ens->sat, dv.as<Real>(), dc.as<Real>())
+    switch (pick_degree(ens->dmax_c)) {
+    case 8: MBP_C2V(8); break;
+    case 16: MBP_C2V(16); break;
+    case 32: MBP_C2V(32); break;
+    case 64: MBP_C2V(64); break;
+    default: return fail(MBP_EUNSUPPORTED, "check degree too large");
+    }
+#undef MBP_C2V
+    MBP_CUDA(cudaGetLastError());
+    MBP_CUDA(cudaMemcpy(hc.data(), dc.p, E * sizeof(Real), cudaMemcpyDeviceToHost));
+    for (size_t k = 0; k < E; ++k) c2v[k] = (double)hc[k];
+    return MBP_OK;
+}
+
+int mbp_c2v_pass(mbp_ensemble* ens, int32_t precision, int32_t matrix_index, const uint8_t* syn_bits,
+                 double clamp, const double* v2c, double* c2v)
+{
+    if (!ens || !syn_bits || !v2c || !c2v) return fail(MBP_EINVAL, "null pointer argument");
+    if (matrix_index < 0 || matrix_index >= ens->u) return fail(MBP_EINVAL, "matrix_index out of range");
+    DeviceGuard dg(ens->device);
+    return precision == MBP_FP64_TANH ? phase_c2v<double>(ens, matrix_index, syn_bits, clamp, v2c, c2v)
+                                      : phase_c2v<float>(ens, matrix_index, syn_bits, clamp, v2c, c2v);
+}
+
+template <class Real>
+static int phase_v2c(mbp_ensemble* ens, int l, int joint, double damping, double clamp, const double* c2v,
+                     const double* priors, double* v2c)
+{
+    const size_t E = ens->E, n = ens->n;
+    std::vector<Real> hc(E), hv(E), hp(n);
+    for (size_t k = 0; k < E; ++k) { hc[k] = (Real)c2v[k]; hv[k] = (Real)v2c[k]; }
+    for (size_t k = 0; k < n; ++k) hp[k] = (Real)priors[k];
+    DevBuf dc, dv, dp;
+    int rc;
+    if ((rc = dc.alloc(E * sizeof(Real))) || (rc = dv.alloc(E * sizeof(Real))) || (rc = dp.alloc(n * sizeof(Real)))) return rc;
+    MBP_CUDA(cudaMemcpy(dc.p, hc.data(), E * sizeof(Real), cudaMemcpyHostToDevice));
+    MBP_CUDA(cudaMemcpy(dv.p, hv.data(), E * sizeof(Real), cudaMemcpyHostToDevice));
+    MBP_CUDA(cudaMemcpy(dp.p, hp.data(), n * sizeof(Real), cudaMemcpyHostToDevice));
+    mbp::v2c_phase_kernel<Real><<<(int)((n + 127) / 128), 128>>>(
+        ens->var_ptr.as<int>(), ens->var_edge.as<int>(), (int)n, (int)ens->edge_off[l], (int)ens->edge_off[l + 1],
+        joint, (Real)damping, (Real)clamp, dc.as<Real>(), dp.as<Real>(), dv.as<Real>());
+    MBP_CUDA(cudaGetLastError());
+    MBP_CUDA(cudaMemcpy(hv.data(), dv.p, E * sizeof(Real), cudaMemcpyDeviceToHost));
+    for (size_t k = 0; k < E; ++k) v2c[k] = (double)hv[k];
+    return MBP_OK;
+}
+
+int mbp_v2c_pass(mbp_ensemble* ens, int32_t precision, int32_t matrix_index, int32_t joint, double damping,
+                 double clamp, const double* c2v, const double* priors, double* v2c)
+{
+    if (!ens || !c2v || !priors || !v2c) return fail(MBP_EINVAL, "null pointer argument");
+    if (matrix_index < 0 || matrix_index >= ens->u) return fail(MBP_EINVAL, "matrix_index out of range");
+    DeviceGuard dg(ens->device);
+    return precision == MBP_FP64_TANH ? phase_v2c<double>(ens, matrix_index, joint, damping, clamp, c2v, priors, v2c)
+                                      : phase_v2c<float>(ens, matrix_index, joint, damping, clamp, c2v, priors, v2c);
+}
+
+template <class Real>
+static int phase_post(mbp_ensemble* ens, const double* c2v, const double* priors, double* post)
+{
+    const size_t E = ens->E, n = ens->n;
+    std::vector<Real> hc(E), hp(n), ho(n);
+    for (size_t k = 0; k < E; ++k) hc[k] = (Real)c2v[k];
+    for (size_t k = 0; k < n; ++k) hp[k] = (Real)priors[k];
+    DevBuf dc, dp, dout;
+    int rc;
+    if ((rc = dc.alloc(E * sizeof(Real))) || (rc = dp.alloc(n * sizeof(Real))) || (rc = dout.alloc(n * sizeof(Real)))) return rc;
+    MBP_CUDA(cudaMemcpy(dc.p, hc.data(), E * sizeof(Real), cudaMemcpyHostToDevice));
+    MBP_CUDA(cudaMemcpy(dp.p, hp.data(), n * sizeof(Real), cudaMemcpyHostToDevice));
+    mbp::posterior_phase_kernel<Real><<<(int)((n + 127) / 128), 128>>>(ens->var_ptr.as<int>(), ens->var_edge.as<int>(),
+                                                                       (int)n, dc.as<Real>(), dp.as<Real>(), dout.as<Real>());
+    MBP_CUDA(cudaGetLastError());
+    MBP_CUDA(cudaMemcpy(ho.data(), dout.p, n * sizeof(Real), cudaMemcpyDeviceToHost));
+    for (size_t k = 0; k < n; ++k) post[k] = (double)ho[k];
+    return MBP_OK;
+}
+
+int mbp_posterior_pass(mbp_ensemble* ens, int32_t precision, const double* c2v, const double* priors, double* posterior)
+{
+    if (!ens || !c2v || !priors || !posterior) return fail(MBP_EINVAL, "null pointer argument");
+    DeviceGuard dg(ens->device);
+    return precision == MBP_FP64_TANH ? phase_post<double>(ens, c2v, priors, posterior)
+                                      : phase_post<float>(ens, c2v, priors, posterior);
+}
+
+void* mbp_host_alloc(size_t bytes)
+{
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        g_last_error = "cudaHostAlloc failed";
+        return nullptr;
+    }
+    return p;
+}
+
+void mbp_host_free(void* p)
+{
+    if (p) cudaFreeHost(p);
+}
+

@@ -1,0 +1,513 @@
+"""Multi-matrix belief-propagation (MBP) decoder on B200 -- the drop-in API.
+
+Same module-level names and semantics as the reference decoder
+(pkg/src/mmrecon/decoder.py:37-274, re-exported at __init__.py:14-21):
+``DecoderConfig``, ``DecodeResult``, ``DecoderWorkspace``,
+``compute_syndrome``, ``init_priors``, ``c2v_update``, ``v2c_update``,
+``soft_decision``, ``decode``, ``reset`` -- with every decode executed by the
+CUDA library (libmbp_b200.so, include/mbp.h).  Added: ``decode_batch`` /
+``syndrome_batch`` and ``BatchDecoder`` for many frames per launch, the way
+the hardware wants to be used.
+
+Numerics: ``DecoderConfig.precision`` selects fp32 messages with Eq. 6 in the
+phi domain (default, the production path) or fp64 messages with the
+reference's literal tanh product ("fp64", parity mode).  Both follow the
+reference's update order and stopping rule; see DESIGN.md §3 for the parity
+contract each meets.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .bits import BitBlock
+from .matrix import stacked_layout
+
+__all__ = [
+    "DecoderConfig",
+    "DecoderWorkspace",
+    "DecodeResult",
+    "BatchResult",
+    "BatchDecoder",
+    "DeviceEnsemble",
+    "compute_syndrome",
+    "init_priors",
+    "c2v_update",
+    "v2c_update",
+    "soft_decision",
+    "decode",
+    "decode_batch",
+    "syndrome_batch",
+    "reset",
+]
+
+COMBINING_MODES = ("joint-graph", "isolated-per-matrix")
+PRECISIONS = ("fp32", "fp64")
+
+
+@dataclass(frozen=True)
+class DecoderConfig:
+    """decoder.py:53-68 plus ``precision`` (device arithmetic)."""
+
+    max_iterations: int = 60
+    llr_clamp: float = 30.0
+    damping: float = 0.0
+    combining_mode: str = "joint-graph"
+    precision: str = "fp32"
+
+    def __post_init__(self):
+        if self.max_iterations < 1:
+            raise ValueError(f"max_iterations must be >= 1, got {self.max_iterations}")
+        if not self.llr_clamp > 0:
+            raise ValueError(f"llr_clamp must be positive, got {self.llr_clamp}")
+        if not 0.0 <= self.damping <= 1.0:
+            raise ValueError(f"damping must be in [0, 1], got {self.damping}")
+        if self.combining_mode not in COMBINING_MODES:
+            raise ValueError(f"combining_mode must be one of {COMBINING_MODES}")
+        if self.precision not in PRECISIONS:
+            raise ValueError(f"precision must be one of {PRECISIONS}")
+
+    def to_c(self, flags: int = 0) -> N.DecoderConfigC:
+        return N.DecoderConfigC(
+            int(self.max_iterations),
+            N.MBP_JOINT_GRAPH if self.combining_mode == "joint-graph" else N.MBP_ISOLATED_PER_MATRIX,
+            N.MBP_FP32_PHI if self.precision == "fp32" else N.MBP_FP64_TANH,
+            int(flags), float(self.llr_clamp), float(self.damping))
+
+
+def _cfg_of(config) -> DecoderConfig:
+    """Accept ours, the reference's DecoderConfig, or None."""
+    if config is None:
+        return DecoderConfig()
+    if isinstance(config, DecoderConfig):
+        return config
+    return DecoderConfig(config.max_iterations, config.llr_clamp, config.damping,
+                         config.combining_mode, getattr(config, "precision", "fp32"))
+
+
+@dataclass(frozen=True)
+class DecodeResult:
+    corrected: BitBlock
+    converged: bool
+    iterations_used: int
+    residual_syndrome_mismatches: int
+    decision_history: np.ndarray | None = None
+
+
+@dataclass
+class BatchResult:
+    """Per-frame outputs of a batched decode (rows are BitBlock bytes)."""
+
+    corrected: np.ndarray    # u8[B, ceil(n/8)]
+    converged: np.ndarray    # bool[B]
+    iterations: np.ndarray   # i32[B]
+    mismatches: np.ndarray   # i32[B]
+    n: int
+
+    def result(self, k: int) -> DecodeResult:
+        return DecodeResult(BitBlock(self.corrected[k].copy(), self.n), bool(self.converged[k]),
+                            int(self.iterations[k]), int(self.mismatches[k]))
+
+
+# ---------------------------------------------------------------------------
+# device objects
+# ---------------------------------------------------------------------------
+
+class DeviceEnsemble:
+    """H_1..H_u uploaded to one GPU as the stacked edge layout (mbp_ensemble)."""
+
+    def __init__(self, ensemble, device: int = 0):
+        self.layout = stacked_layout(ensemble)
+        lay = self.layout
+        self.n, self.m, self.u = lay.n, lay.m, lay.u
+        self.device = int(device)
+        self._ensemble = ensemble
+        handle = C.c_void_p()
+        chk_ptr = np.ascontiguousarray(lay.chk_ptr, dtype=np.int64)
+        chk_var = np.ascontiguousarray(lay.chk_var, dtype=np.int32)
+        N.call("mbp_ensemble_create", lay.n, lay.m, lay.u, chk_ptr.ctypes.data,
+               chk_var.ctypes.data, self.device, C.byref(handle))
+        self.handle = handle
+        info = N.EnsembleInfoC()
+        N.call("mbp_ensemble_get_info", self.handle, C.byref(info))
+        self.info = info
+
+    @property
+    def nbytes_key(self) -> int:
+        return (self.n + 7) // 8
+
+    @property
+    def nbytes_syn(self) -> int:
+        return self.u * ((self.m + 7) // 8)
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h and N._LIB is not None:
+            N._LIB.mbp_ensemble_destroy(h)
+            self.handle = None
+
+
+_DEV_CACHE: dict = {}
+_DEV_LOCK = threading.Lock()
+
+
+def device_ensemble(ensemble, device: int = 0) -> DeviceEnsemble:
+    """Upload once per (ensemble object, device); the ensemble is immutable."""
+    if isinstance(ensemble, DeviceEnsemble):
+        return ensemble
+    key = (id(ensemble), int(device))
+    with _DEV_LOCK:
+        de = _DEV_CACHE.get(key)
+        if de is None or de._ensemble is not ensemble:
+            de = DeviceEnsemble(ensemble, device)
+            _DEV_CACHE[key] = de
+        return de
+
+
+class BatchDecoder:
+    """A device workspace for up to ``max_frames`` frames (mbp_workspace).
+
+    ``decode`` takes numpy rows (host path: copies in, decodes, copies out,
+    synchronises) or CUDA tensors (device path: enqueued on the current torch
+    stream, no synchronisation)."""
+
+    def __init__(self, ensemble, max_frames: int, config=None, device: int = 0, flags: int = 0):
+        self.dev = device_ensemble(ensemble, device)
+        self.config = _cfg_of(config)
+        self.flags = int(flags)
+        self.max_frames = int(max_frames)
+        handle = C.c_void_p()
+        cfg = self.config.to_c(self.flags)
+        N.call("mbp_workspace_create", self.dev.handle, self.max_frames, C.byref(cfg), C.byref(handle))
+        self.handle = handle
+
+    def configure(self, config=None, flags: int | None = None) -> None:
+        config = _cfg_of(config)
+        if flags is not None:
+            self.flags = int(flags)
+        cfg = config.to_c(self.flags)
+        N.call("mbp_workspace_configure", self.handle, C.byref(cfg))
+        self.config = config
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h and N._LIB is not None:
+            N._LIB.mbp_workspace_destroy(h)
+            self.handle = None
+
+    # -- host buffers -------------------------------------------------------
+    def _check_rows(self, noisy, syn):
+        B = noisy.shape[0]
+        if noisy.shape != (B, self.dev.nbytes_key):
+            raise ValueError(f"noisy rows must be [B, {self.dev.nbytes_key}] bytes, got {tuple(noisy.shape)}")
+        if syn.shape != (B, self.dev.nbytes_syn):
+            raise ValueError(f"syndrome rows must be [B, {self.dev.nbytes_syn}] bytes, got {tuple(syn.shape)}")
+        return B
+
+    def decode(self, noisy, syn, e, out=None, stream=None) -> BatchResult:
+        if hasattr(noisy, "is_cuda") and noisy.is_cuda:
+            return self.decode_device(noisy, syn, e, out=out, stream=stream)
+        noisy = np.ascontiguousarray(noisy, dtype=np.uint8)
+        syn = np.ascontiguousarray(syn, dtype=np.uint8)
+        B = self._check_rows(noisy, syn)
+        ev = np.ascontiguousarray(np.asarray(e, dtype=np.float64).reshape(-1))
+        if ev.size not in (1, B):
+            raise ValueError("e must be a scalar or one value per frame")
+        if np.any(~((ev > 0.0) & (ev < 0.5))):
+            raise ValueError(f"crossover probability must be in (0, 0.5), got {ev[(ev <= 0) | (ev >= 0.5)][0]}")
+        if out is None:
+            out = BatchResult(np.empty_like(noisy), np.empty(B, dtype=np.uint8),
+                              np.empty(B, dtype=np.int32), np.empty(B, dtype=np.int32), self.dev.n)
+        N.call("mbp_decode_batch", self.handle, noisy.ctypes.data, syn.ctypes.data, ev.ctypes.data,
+               0 if ev.size == 1 else 1, B, N.ptr(out.corrected), N.ptr(out.converged),
+               N.ptr(out.iterations), N.ptr(out.mismatches))
+        out.converged = out.converged.astype(bool)
+        return out
+
+    def decode_device(self, noisy, syn, e, out=None, stream=None):
+        """CUDA-tensor path (inputs resident in HBM); returns device tensors."""
+        import torch
+
+        B = self._check_rows(noisy, syn)
+        if not torch.is_tensor(e):
+            e = torch.tensor([float(e)], dtype=torch.float64, device=noisy.device)
+        if out is None:
+            out = (torch.empty_like(noisy), torch.empty(B, dtype=torch.uint8, device=noisy.device),
+                   torch.empty(B, dtype=torch.int32, device=noisy.device),
+                   torch.empty(B, dtype=torch.int32, device=noisy.device))
+        s = stream if stream is not None else torch.cuda.current_stream(noisy.device).cuda_stream
+        N.call("mbp_decode_batch_device", self.handle, noisy.data_ptr(), syn.data_ptr(), e.data_ptr(),
+               0 if e.numel() == 1 else 1, B, out[0].data_ptr(), out[1].data_ptr(), out[2].data_ptr(),
+               out[3].data_ptr(), C.c_void_p(s))
+        return out
+
+    def syndromes(self, keys, out=None, stream=None):
+        """Alice side, Eq. 1 for all u matrices: rows [B, u*ceil(m/8)]."""
+        if hasattr(keys, "is_cuda") and keys.is_cuda:
+            import torch
+
+            B = keys.shape[0]
+            if out is None:
+                out = torch.empty((B, self.dev.nbytes_syn), dtype=torch.uint8, device=keys.device)
+            s = stream if stream is not None else torch.cuda.current_stream(keys.device).cuda_stream
+            N.call("mbp_syndrome_batch_device", self.handle, keys.data_ptr(), B, out.data_ptr(), C.c_void_p(s))
+            return out
+        keys = np.ascontiguousarray(keys, dtype=np.uint8)
+        B = keys.shape[0]
+        if keys.shape != (B, self.dev.nbytes_key):
+            raise ValueError(f"key rows must be [B, {self.dev.nbytes_key}] bytes")
+        out = np.empty((B, self.dev.nbytes_syn), dtype=np.uint8) if out is None else out
+        N.call("mbp_syndrome_batch", self.handle, keys.ctypes.data, B, out.ctypes.data)
+        return out
+
+    # -- state of the last decode ----------------------------------------------
+    def posterior(self, k: int) -> np.ndarray:
+        out = np.empty(self.dev.n, dtype=np.float64)
+        N.call("mbp_workspace_read_posterior", self.handle, int(k), out.ctypes.data)
+        return out
+
+    def c2v(self, k: int) -> np.ndarray:
+        out = np.empty(self.dev.layout.edges, dtype=np.float64)
+        N.call("mbp_workspace_read_c2v", self.handle, int(k), out.ctypes.data)
+        return out
+
+    def v2c_previous(self, k: int) -> np.ndarray:
+        out = np.empty(self.dev.layout.edges, dtype=np.float64)
+        N.call("mbp_workspace_read_v2c", self.handle, int(k), out.ctypes.data)
+        return out
+
+    def history(self, k: int, rows: int) -> np.ndarray:
+        nb = self.dev.nbytes_key
+        out = np.zeros((rows, nb), dtype=np.uint8)
+        N.call("mbp_workspace_read_history", self.handle, int(k), int(rows), out.ctypes.data)
+        return np.unpackbits(out, axis=1, count=self.dev.n, bitorder="little")
+
+    def last_timing(self, e2e: bool = False):
+        """(decode-kernel ms, sweeps run) of the last decode; with e2e=True
+        also the device-timed ms of the last host-buffer call."""
+        ms = C.c_float(0.0)
+        e2 = C.c_float(0.0)
+        sw = C.c_int32(0)
+        N.call("mbp_workspace_last_timing", self.handle, C.byref(ms), C.byref(e2) if e2e else None,
+               C.byref(sw))
+        if e2e:
+            return float(ms.value), float(e2.value), int(sw.value)
+        return float(ms.value), int(sw.value)
+
+
+def decode_batch(ensemble, noisy_rows, syn_rows, e, config=None, device: int = 0) -> BatchResult:
+    """Decode B frames in one launch (host rows in, host rows out)."""
+    noisy_rows = np.ascontiguousarray(noisy_rows, dtype=np.uint8)
+    dec = BatchDecoder(ensemble, max(noisy_rows.shape[0], 1), config, device)
+    return dec.decode(noisy_rows, syn_rows, e)
+
+
+def syndrome_batch(ensemble, key_rows, device: int = 0) -> np.ndarray:
+    key_rows = np.ascontiguousarray(key_rows, dtype=np.uint8)
+    dec = BatchDecoder(ensemble, max(key_rows.shape[0], 1), None, device)
+    return dec.syndromes(key_rows)
+
+
+# ---------------------------------------------------------------------------
+# reference API mirror
+# ---------------------------------------------------------------------------
+
+class DecoderWorkspace:
+    """Per-frame message buffers for one ensemble (decoder.py:80-134).
+
+    Host float64 arrays with the reference's stacked layout; after ``decode``
+    they mirror the device state (posterior, c2v, v2c, hard).  The device
+    buffers live in a ``BatchDecoder`` of capacity one frame."""
+
+    def __init__(self, ensemble, config=None):
+        self.ensemble = ensemble
+        self.config = _cfg_of(config)
+        lay = stacked_layout(ensemble)
+        self.layout = lay
+        self.edge_off = lay.edge_off
+        self.chk_ptr = lay.chk_ptr
+        self.chk_var = lay.chk_var
+        self.var_ptr = lay.var_ptr
+        self.var_edge = lay.var_edge
+        total = lay.edges
+        n = lay.n
+        self.v2c = np.zeros(total, dtype=np.float64)
+        self.c2v = np.zeros(total, dtype=np.float64)
+        self.priors = np.zeros(n, dtype=np.float64)
+        self.posterior = np.zeros(n, dtype=np.float64)
+        self.hard = np.zeros(n, dtype=np.uint8)
+        self.iteration = 0
+        self._dec = None
+        self._dec_key = None
+
+    def reset(self) -> None:
+        self.v2c[:] = 0.0
+        self.c2v[:] = 0.0
+        self.priors[:] = 0.0
+        self.posterior[:] = 0.0
+        self.hard[:] = 0
+        self.iteration = 0
+
+    def matrix_slice(self, l: int) -> slice:
+        return slice(int(self.edge_off[l]), int(self.edge_off[l + 1]))
+
+    def _device(self, config: DecoderConfig, track: bool) -> BatchDecoder:
+        flags = N.MBP_KEEP_STATE | (N.MBP_RECORD_HISTORY if track else 0)
+        shape_key = (config.precision, config.combining_mode)
+        if self._dec is None or self._dec_key != shape_key:
+            self._dec = BatchDecoder(self.ensemble, 1, config, flags=flags)
+            self._dec_key = shape_key
+        elif self._dec.config != config or self._dec.flags != flags:
+            self._dec.configure(config, flags)
+        return self._dec
+
+
+def _matrices(ensemble_or_matrix):
+    return tuple(getattr(ensemble_or_matrix, "matrices", (ensemble_or_matrix,)))
+
+
+def compute_syndrome(matrix, key) -> BitBlock:
+    """z_j = XOR of key bits over check j (Eq. 1) -- on the GPU."""
+    if key.length != matrix.n:
+        raise ValueError(f"key length {key.length} != n={matrix.n}")
+    dec = _syndrome_decoder(matrix)
+    rows = dec.syndromes(np.asarray(key.data, dtype=np.uint8).reshape(1, -1))
+    return BitBlock(rows[0, : (matrix.m + 7) // 8].copy(), matrix.m)
+
+
+_SYN_CACHE: dict = {}
+
+
+def _syndrome_decoder(matrix) -> BatchDecoder:
+    key = id(matrix)
+    dec = _SYN_CACHE.get(key)
+    if dec is None or dec.dev._ensemble is not matrix:
+        dec = BatchDecoder(matrix, 32)
+        _SYN_CACHE[key] = dec
+    return dec
+
+
+def init_priors(noisy_key, e: float) -> np.ndarray:
+    """(1 - 2 y_i) ln((1-e)/e) (Eq. 5; decoder.py:147-152).  Host helper: the
+    device decode forms the same prior itself from the packed noisy key."""
+    if not 0.0 < e < 0.5:
+        raise ValueError(f"crossover probability must be in (0, 0.5), got {e}")
+    bits = noisy_key.to_bits().astype(np.float64)
+    return (1.0 - 2.0 * bits) * math.log((1.0 - e) / e)
+
+
+def _precision_code(ws) -> int:
+    return N.MBP_FP64_TANH if ws.config.precision == "fp64" else N.MBP_FP32_PHI
+
+
+def c2v_update(workspace: DecoderWorkspace, matrix_index: int, syndrome) -> None:
+    """Recompute matrix ``matrix_index``'s c2v messages from ws.v2c (Eq. 6)."""
+    m = workspace.layout.m
+    if syndrome.length != m:
+        raise ValueError(f"syndrome length {syndrome.length} != m={m}")
+    dev = device_ensemble(workspace.ensemble)
+    syn = np.ascontiguousarray(syndrome.to_bits(), dtype=np.uint8)
+    N.call("mbp_c2v_pass", dev.handle, _precision_code(workspace), int(matrix_index), syn.ctypes.data,
+           float(workspace.config.llr_clamp), workspace.v2c.ctypes.data, workspace.c2v.ctypes.data)
+
+
+def v2c_update(workspace: DecoderWorkspace, matrix_index: int) -> None:
+    cfg = workspace.config
+    dev = device_ensemble(workspace.ensemble)
+    N.call("mbp_v2c_pass", dev.handle, _precision_code(workspace), int(matrix_index),
+           int(cfg.combining_mode == "joint-graph"), float(cfg.damping), float(cfg.llr_clamp),
+           workspace.c2v.ctypes.data, workspace.priors.ctypes.data, workspace.v2c.ctypes.data)
+
+
+def soft_decision(workspace: DecoderWorkspace) -> np.ndarray:
+    """Posterior LLR (Eq. 2): prior + every matrix's c2v."""
+    dev = device_ensemble(workspace.ensemble)
+    N.call("mbp_posterior_pass", dev.handle, _precision_code(workspace), workspace.c2v.ctypes.data,
+           workspace.priors.ctypes.data, workspace.posterior.ctypes.data)
+    return workspace.posterior
+
+
+def reset(workspace: DecoderWorkspace) -> None:
+    workspace.reset()
+
+
+def _same_ensemble(a, b) -> bool:
+    if a is b:
+        return True
+    ma, mb = _matrices(a), _matrices(b)
+    return len(ma) == len(mb) and all(x == y for x, y in zip(ma, mb))
+
+
+def decode(ensemble, noisy_key, syndromes, e: float, config=None, workspace=None,
+           track_decisions: bool = False) -> DecodeResult:
+    """Correct ``noisy_key`` toward the key behind ``syndromes`` (decoder.py:207-274).
+
+    A batch-of-one call of the device decoder; the workspace's host arrays
+    mirror the final device state as the reference's would."""
+    config = _cfg_of(config)
+    mats = _matrices(ensemble)
+    n, m, u = mats[0].n, mats[0].m, len(mats)
+    if noisy_key.length != n:
+        raise ValueError(f"key length {noisy_key.length} != n={n}")
+    if len(syndromes) != u:
+        raise ValueError(f"{len(syndromes)} syndromes for u={u} matrices")
+    for l, z in enumerate(syndromes):
+        if z.length != m:
+            raise ValueError(f"syndrome {l} length {z.length} != m={m}")
+    if workspace is None:
+        workspace = DecoderWorkspace(ensemble, config)
+    elif not _same_ensemble(workspace.ensemble, ensemble):
+        raise ValueError("workspace was built for a different ensemble")
+    workspace.config = config
+    workspace.reset()
+    workspace.priors[:] = init_priors(noisy_key, e)
+
+    dec = workspace._device(config, track_decisions)
+    noisy = np.asarray(noisy_key.data, dtype=np.uint8).reshape(1, -1)
+    syn = np.concatenate([np.asarray(z.data, dtype=np.uint8) for z in syndromes]).reshape(1, -1)
+    res = dec.decode(noisy, syn, e)
+    iters = int(res.iterations[0])
+
+    # mirror the device state into the reference-layout host arrays
+    lay = workspace.layout
+    workspace.hard[:] = np.unpackbits(res.corrected[0], count=n, bitorder="little")
+    if iters == 0:
+        workspace.v2c[:] = workspace.priors[lay.chk_var]
+    else:
+        workspace.c2v[:] = dec.c2v(0)
+        workspace.posterior[:] = dec.posterior(0)
+        workspace.v2c[:] = _final_v2c(workspace, config, dec)
+    workspace.iteration = iters
+    history = dec.history(0, iters + 1) if track_decisions else None
+    return DecodeResult(
+        corrected=BitBlock(res.corrected[0].copy(), n),
+        converged=bool(res.converged[0]),
+        iterations_used=iters,
+        residual_syndrome_mismatches=int(res.mismatches[0]),
+        decision_history=history,
+    )
+
+
+def _final_v2c(ws: DecoderWorkspace, cfg: DecoderConfig, dec: BatchDecoder) -> np.ndarray:
+    """v2c after the last sweep's v2c_pass (_kernels.py:264-290), from the
+    device's final c2v/posterior (and previous v2c when damping)."""
+    lay = ws.layout
+    if cfg.combining_mode == "joint-graph":
+        total_e = ws.posterior[lay.chk_var]
+    else:
+        total_e = np.empty(lay.edges)
+        for l in range(lay.u):
+            sl = ws.matrix_slice(l)
+            tot = ws.priors.copy()
+            np.add.at(tot, lay.chk_var[sl], ws.c2v[sl])
+            total_e[sl] = tot[lay.chk_var[sl]]
+    val = total_e - ws.c2v
+    if cfg.damping != 0.0:
+        val = (1.0 - cfg.damping) * val + cfg.damping * dec.v2c_previous(0)
+    return np.clip(val, -cfg.llr_clamp, cfg.llr_clamp)
