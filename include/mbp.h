@@ -63,7 +63,8 @@ typedef enum {
 } mbp_precision;
 enum {
     MBP_RECORD_HISTORY = 1,  /* keep the hard decision after every sweep     */
-    MBP_KEEP_STATE = 2       /* keep posteriors/messages readable after decode */
+    MBP_KEEP_STATE = 2,      /* keep posteriors/messages readable after decode */
+    MBP_PROFILE_PHASES = 4   /* record a globaltimer stamp at every phase barrier */
 };
 
 typedef struct mbp_decoder_config {
@@ -146,6 +147,11 @@ int mbp_workspace_read_c2v(mbp_workspace *ws, int64_t frame, double *c2v_E);
 int mbp_workspace_read_v2c(mbp_workspace *ws, int64_t frame, double *v2c_E);
 /* rows [0, rows) of frame's decision history, packed [rows][ceil(n/8)] */
 int mbp_workspace_read_history(mbp_workspace *ws, int64_t frame, int32_t rows, uint8_t *out);
+
+/* globaltimer (ns) stamps of the last decode's chunk (MBP_PROFILE_PHASES):
+ * kernel start, then after each grid barrier (3 per executed sweep: check,
+ * variable, syndrome phases, plus the final stop test), then kernel end.  */
+int mbp_workspace_read_phase_times(mbp_workspace *ws, uint64_t *ns, int32_t cap, int32_t *count);
 
 /* ---- single phases on explicit per-edge messages of ONE frame ------------
  * (decoder.py:155-200).  Host arrays in the reference's float64 layout:

@@ -15,7 +15,7 @@ from .build import LIB
 MBP_OK, MBP_EINVAL, MBP_ECUDA, MBP_EUNSUPPORTED, MBP_ENOMEM = range(5)
 MBP_JOINT_GRAPH, MBP_ISOLATED_PER_MATRIX = 0, 1
 MBP_FP32_PHI, MBP_FP64_TANH = 0, 1
-MBP_RECORD_HISTORY, MBP_KEEP_STATE = 1, 2
+MBP_RECORD_HISTORY, MBP_KEEP_STATE, MBP_PROFILE_PHASES = 1, 2, 4
 
 #: every symbol include/mbp.h declares (checked by tests/test_native_abi.py)
 EXPORTS = (
@@ -25,7 +25,7 @@ EXPORTS = (
     "mbp_syndrome_batch_device", "mbp_syndrome_batch",
     "mbp_decode_batch_device", "mbp_decode_batch",
     "mbp_workspace_read_posterior", "mbp_workspace_read_c2v", "mbp_workspace_read_v2c",
-    "mbp_workspace_read_history",
+    "mbp_workspace_read_history", "mbp_workspace_read_phase_times",
     "mbp_c2v_pass", "mbp_v2c_pass", "mbp_posterior_pass",
     "mbp_host_alloc", "mbp_host_free", "mbp_workspace_last_timing",
 )
@@ -70,6 +70,7 @@ _SIGS = {
     "mbp_workspace_read_c2v": ([_VP, C.c_int64, _VP], C.c_int),
     "mbp_workspace_read_v2c": ([_VP, C.c_int64, _VP], C.c_int),
     "mbp_workspace_read_history": ([_VP, C.c_int64, C.c_int32, _VP], C.c_int),
+    "mbp_workspace_read_phase_times": ([_VP, _VP, C.c_int32, C.POINTER(C.c_int32)], C.c_int),
     "mbp_c2v_pass": ([_VP, C.c_int32, C.c_int32, _VP, C.c_double, _VP, _VP], C.c_int),
     "mbp_v2c_pass": ([_VP, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_double, _VP, _VP, _VP], C.c_int),
     "mbp_posterior_pass": ([_VP, C.c_int32, _VP, _VP, _VP], C.c_int),

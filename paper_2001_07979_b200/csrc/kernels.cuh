@@ -73,9 +73,34 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar)
 // rounds to exactly 1.0, and all-others-saturated then gives +-clamp as in
 // the `prod >= 1.0` branch of c2v_pass (_kernels.py:249-252).
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ float ex2_approx(float x)
+{
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float lg2_approx(float x)
+{
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// phi(x) = ln((1+t)/(1-t)), t = e^-x, branch-free, 3 MUFU + ~16 FMA, max
+// relative error ~7e-7 over [0, inf] (phi(0) = inf, phi(inf) = 0):
+//   1 - t from its Taylor series below x = 1/4 (no cancellation),
+//   2 atanh(t) series once t < 1/8 (no lg2 of a ratio near 1).
 __device__ __forceinline__ float phi_f32(float x)
 {
-    return log1pf(2.0f / expm1f(x));
+    const float t = ex2_approx(-1.44269504088896341f * x);
+    const float dser = x * (1.0f - x * (0.5f - x * (1.0f / 6 - x * (1.0f / 24 - x * (1.0f / 120 - x * (1.0f / 720))))));
+    const float den = x < 0.25f ? dser : 1.0f - t;
+    const float num = 2.0f - den;
+    const float L = (lg2_approx(num) - lg2_approx(den)) * 0.69314718055994531f;
+    const float t2 = t * t;
+    const float ser = 2.0f * t * (1.0f + t2 * (1.0f / 3 + t2 * (1.0f / 5 + t2 * (1.0f / 7 + t2 * (1.0f / 9)))));
+    return t < 0.125f ? ser : L;
 }
 
 template <int D> struct SignMask { using T = unsigned; };
@@ -152,23 +177,32 @@ template <class Real> __device__ __forceinline__ Real clampr(Real v, Real c)
 
 // ---------------------------------------------------------------------------
 // decode kernel arguments
+//
+// Internal edge numbering (padded ELL): edge k of stacked check j is slot
+// j*D + k, D = the kernel's degree bound.  A check's var ids chk_ell[j*D..]
+// and its message lines are contiguous and need no chk_ptr lookup (one
+// dependent load less per item); slot order is monotone in the reference's
+// edge order, so ascending var_edge lists and matrix boundaries
+// (edge_off[l] = l*m*D) keep the reference's summation order.
 // ---------------------------------------------------------------------------
 template <class Real>
 struct DecodeArgs {
-    // graph (stacked, int32 indices)
-    int n, m, u, C, E;
-    const int* __restrict__ chk_ptr;   // [C+1]
-    const int* __restrict__ chk_var;   // [E]
-    const int* __restrict__ var_ptr;   // [n+1]
-    const int* __restrict__ var_edge;  // [E]
-    int edge_off[kMaxU + 1];
+    // graph
+    int n, m, u, C;
+    long long slots;                   // C * D
+    const uint8_t* __restrict__ deg;   // [C] row degree
+    const int* __restrict__ chk_ell;   // [C*D] var ids (pad 0)
+    const int* __restrict__ var_ptr;   // [n+1] into var_edge (CSR; unused when dv > 0)
+    const int* __restrict__ var_edge;  // [E] slot ids, ascending per variable
+    int dv;                            // regular column degree, 0 if irregular
+    long long edge_off[kMaxU + 1];     // slot offsets of the matrices
     // batch
     int G;                       // groups of 32 frames
     // state
-    Real* __restrict__ c2v;      // [G][E][32]
+    Real* __restrict__ c2v;      // [G][slots][32]
     Real* __restrict__ post;     // [G][P][n][32], P = ISO ? u+1 : 1
-    Real* __restrict__ v2c;      // [G][E][32] (damping only)
-    const Real* __restrict__ Lmag;      // [G*32] prior magnitude per frame
+    Real* __restrict__ v2c;      // [G][slots][32] (damping only)
+    const Real* __restrict__ Lmag;         // [G*32] prior magnitude per frame
     const unsigned* __restrict__ noisy_w;  // [G][n]
     const unsigned* __restrict__ syn_w;    // [G][C]
     unsigned* __restrict__ hard_w;         // [G][n]
@@ -178,6 +212,8 @@ struct DecodeArgs {
     int* __restrict__ iters;     // [G*32] first converged sweep, -1 unset
     unsigned* __restrict__ barrier;  // [2]
     int* __restrict__ sweeps_run;    // [1]
+    unsigned long long* __restrict__ ts;  // phase timestamps (globaltimer ns) or null
+    int ts_cap;
     // outputs (per frame, batch B)
     int B;
     uint8_t* __restrict__ out_conv;
@@ -196,18 +232,18 @@ template <class Real, int D, bool DAMP, bool ISO>
 __device__ __forceinline__ void check_item(const DecodeArgs<Real>& A, int g, int j, int t,
                                            unsigned act, int lane)
 {
-    const int e0 = ld_ro(A.chk_ptr + j);
-    const int d = ld_ro(A.chk_ptr + j + 1) - e0;
+    const int d = ld_ro(A.deg + j);
     constexpr int NC = (D + 31) / 32;
     int vid[NC];
 #pragma unroll
-    for (int c = 0; c < NC; ++c) vid[c] = (c * 32 + lane < d) ? ld_ro(A.chk_var + e0 + c * 32 + lane) : 0;
+    for (int c = 0; c < NC; ++c)
+        vid[c] = (c * 32 + lane < D) ? ld_ro(A.chk_ell + (size_t)j * D + c * 32 + lane) : 0;
     const bool live = (act >> lane) & 1u;
     const unsigned flip = (ld_ro(A.syn_w + (size_t)g * A.C + j) >> lane) & 1u;
     const Real L = ld_ro(A.Lmag + g * 32 + lane);
     const int mat = ISO ? j / A.m : 0;
-    const size_t lineE = (size_t)g * A.E + e0;
-    const Real* postg = A.post + ((size_t)g * (ISO ? A.u + 1 : 1) + mat) * A.n * 32;
+    const size_t line0 = ((size_t)g * A.slots + (size_t)j * D) * 32 + lane;
+    const Real* postg = A.post + ((size_t)g * (ISO ? A.u + 1 : 1) + mat) * A.n * 32 + lane;
 
     Real x[D];
     if (t == 1) {
@@ -215,17 +251,16 @@ __device__ __forceinline__ void check_item(const DecodeArgs<Real>& A, int g, int
         const unsigned* nw = A.noisy_w + (size_t)g * A.n;
 #pragma unroll
         for (int k = 0; k < D; ++k) {
+            x[k] = Real(0);
             if (k < d) {
                 const int v = __shfl_sync(kFull, vid[k >> 5], k & 31);
                 x[k] = ((ld_ro(nw + v) >> lane) & 1u) ? -L : L;
-            } else {
-                x[k] = Real(0);
             }
         }
         if (DAMP && live) {
 #pragma unroll
             for (int k = 0; k < D; ++k)
-                if (k < d) A.v2c[(lineE + k) * 32 + lane] = x[k];
+                if (k < d) A.v2c[line0 + (size_t)k * 32] = x[k];
         }
     } else {
         Real p[D], q[D];
@@ -236,8 +271,8 @@ __device__ __forceinline__ void check_item(const DecodeArgs<Real>& A, int g, int
             if (k < d) {
                 const int v = __shfl_sync(kFull, vid[k >> 5], k & 31);
                 if (live) {
-                    p[k] = ld_cg(postg + (size_t)v * 32 + lane);
-                    q[k] = ld_cg(A.c2v + (lineE + k) * 32 + lane);
+                    p[k] = ld_cg(postg + (size_t)v * 32);
+                    q[k] = ld_cg(A.c2v + line0 + (size_t)k * 32);
                 }
             }
         }
@@ -246,7 +281,7 @@ __device__ __forceinline__ void check_item(const DecodeArgs<Real>& A, int g, int
             Real val = p[k] - q[k];
             if (DAMP) {
                 if (k < d && live) {
-                    const Real old = ld_cg(A.v2c + (lineE + k) * 32 + lane);
+                    const Real old = ld_cg(A.v2c + line0 + (size_t)k * 32);
                     val = (Real(1) - A.damping) * val + A.damping * old;
                 }
             }
@@ -255,7 +290,7 @@ __device__ __forceinline__ void check_item(const DecodeArgs<Real>& A, int g, int
         if (DAMP && live) {
 #pragma unroll
             for (int k = 0; k < D; ++k)
-                if (k < d) A.v2c[(lineE + k) * 32 + lane] = x[k];
+                if (k < d) A.v2c[line0 + (size_t)k * 32] = x[k];
         }
     }
     Real out[D];
@@ -263,7 +298,7 @@ __device__ __forceinline__ void check_item(const DecodeArgs<Real>& A, int g, int
     if (live) {
 #pragma unroll
         for (int k = 0; k < D; ++k)
-            if (k < d) A.c2v[(lineE + k) * 32 + lane] = out[k];
+            if (k < d) A.c2v[line0 + (size_t)k * 32] = out[k];
     }
 }
 
@@ -275,13 +310,15 @@ template <class Real, bool ISO>
 __device__ __forceinline__ void var_item(const DecodeArgs<Real>& A, int g, int i, int t,
                                          unsigned act, int lane)
 {
-    const int p0 = ld_ro(A.var_ptr + i);
-    const int dv = ld_ro(A.var_ptr + i + 1) - p0;
+    const int p0 = A.dv ? i * A.dv : ld_ro(A.var_ptr + i);
+    const int dv = A.dv ? A.dv : ld_ro(A.var_ptr + i + 1) - p0;
     const bool live = (act >> lane) & 1u;
-    const unsigned nwd = ld_ro(A.noisy_w + (size_t)g * A.n + i);
+    const size_t w = (size_t)g * A.n + i;
+    const unsigned nwd = ld_ro(A.noisy_w + w);
+    const unsigned old = lane == 0 ? ld_cg(A.hard_w + w) : 0u;
     const Real L = ld_ro(A.Lmag + g * 32 + lane);
     const Real prior = ((nwd >> lane) & 1u) ? -L : L;
-    const Real* c2vg = A.c2v + (size_t)g * A.E * 32 + lane;
+    const Real* c2vg = A.c2v + (size_t)g * A.slots * 32 + lane;
     Real acc = prior;
     if (!ISO) {
         for (int base = 0; base < dv; base += 32) {
@@ -313,7 +350,7 @@ __device__ __forceinline__ void var_item(const DecodeArgs<Real>& A, int g, int i
                 }
             }
         }
-        if (live) A.post[((size_t)g * A.n + i) * 32 + lane] = acc;
+        if (live) A.post[w * 32 + lane] = acc;
     } else {
         const size_t P = (size_t)(A.u + 1);
         Real part = prior;
@@ -341,8 +378,6 @@ __device__ __forceinline__ void var_item(const DecodeArgs<Real>& A, int g, int i
     }
     const unsigned neg = __ballot_sync(kFull, acc < Real(0));
     if (lane == 0) {
-        const size_t w = (size_t)g * A.n + i;
-        const unsigned old = ld_cg(A.hard_w + w);
         const unsigned hw = (neg & act) | (old & ~act);
         A.hard_w[w] = hw;
         if (A.hist_w) A.hist_w[((size_t)t * A.G) * A.n + w] = hw;
@@ -352,7 +387,7 @@ __device__ __forceinline__ void var_item(const DecodeArgs<Real>& A, int g, int i
 // Syndrome phase item: 32 consecutive checks (lane = check) of group g.
 // Mismatch words (bit f = frame f) are turned into per-frame counts with 32
 // ballots and added to cnt[t&1].
-template <class Real>
+template <class Real, int D>
 __device__ __forceinline__ void syncheck_item(const DecodeArgs<Real>& A, int g, int blk, int t,
                                               unsigned act, int lane)
 {
@@ -360,9 +395,10 @@ __device__ __forceinline__ void syncheck_item(const DecodeArgs<Real>& A, int g, 
     unsigned mism = 0;
     if (j < A.C) {
         const unsigned* hw = A.hard_w + (size_t)g * A.n;
-        const int a0 = ld_ro(A.chk_ptr + j), a1 = ld_ro(A.chk_ptr + j + 1);
+        const int d = ld_ro(A.deg + j);
+        const int* row = A.chk_ell + (size_t)j * D;
         unsigned par = 0;
-        for (int a = a0; a < a1; ++a) par ^= ld_cg(hw + ld_ro(A.chk_var + a));
+        for (int k = 0; k < d; ++k) par ^= ld_cg(hw + ld_ro(row + k));
         mism = (par ^ ld_ro(A.syn_w + (size_t)g * A.C + j)) & act;
     }
     int c = 0;
@@ -373,6 +409,20 @@ __device__ __forceinline__ void syncheck_item(const DecodeArgs<Real>& A, int g, 
     }
     if (c) atomicAdd(A.cnt + (t & 1) * A.G * 32 + g * 32 + lane, c);
     if (__any_sync(kFull, c != 0) && lane == 0) atomicOr(A.any_bad + (t & 1), 1);
+}
+
+__device__ __forceinline__ unsigned long long globaltimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <class Real>
+__device__ __forceinline__ void stamp(const DecodeArgs<Real>& A, int& k)
+{
+    if (A.ts && blockIdx.x == 0 && threadIdx.x == 0 && k < A.ts_cap) A.ts[k] = globaltimer();
+    ++k;
 }
 
 template <class Real, int D>
@@ -392,15 +442,18 @@ decode_kernel(const DecodeArgs<Real> A)
     const int nthreads = gridDim.x * blockDim.x;
     const int F = A.G * 32;
     const int cblk = (A.C + 31) / 32;
+    int ts_k = 0;
+    stamp(A, ts_k);
 
     // iteration 0: the uncorrected key against all u*m syndromes (_kernels.py:358-365)
     for (int item = gw; item < A.G * cblk; item += nw)
-        syncheck_item<Real>(A, item / cblk, item % cblk, 0, kFull, lane);
+        syncheck_item<Real, D>(A, item / cblk, item % cblk, 0, kFull, lane);
 
     int t = 1;
     int final_t = 0;
     for (;; ++t) {
         grid_barrier(A.barrier);
+        stamp(A, ts_k);
         const int* cprev = A.cnt + ((t - 1) & 1) * F;
         // frames whose sweep t-1 decision satisfied every syndrome stop here
         for (int f = gtid; f < F; f += nthreads) {
@@ -413,22 +466,39 @@ decode_kernel(const DecodeArgs<Real> A)
         }
         if (gtid == 0) A.any_bad[t & 1] = 0;
 
+        // the active-frame mask of a group is cached per warp: grid-stride
+        // items of a warp stay in one group for many consecutive items
+        int gc = -1;
+        unsigned act = 0;
         for (int item = gw; item < A.G * A.C; item += nw) {
             const int g = item / A.C;
-            const unsigned act = __ballot_sync(kFull, ld_cg(cprev + g * 32 + lane) != 0);
+            if (g != gc) {
+                act = __ballot_sync(kFull, ld_cg(cprev + g * 32 + lane) != 0);
+                gc = g;
+            }
             if (act) check_item<Real, D, DAMP, ISO>(A, g, item - g * A.C, t, act, lane);
         }
         grid_barrier(A.barrier);
+        stamp(A, ts_k);
+        gc = -1;
         for (int item = gw; item < A.G * A.n; item += nw) {
             const int g = item / A.n;
-            const unsigned act = __ballot_sync(kFull, ld_cg(cprev + g * 32 + lane) != 0);
+            if (g != gc) {
+                act = __ballot_sync(kFull, ld_cg(cprev + g * 32 + lane) != 0);
+                gc = g;
+            }
             if (act) var_item<Real, ISO>(A, g, item - g * A.n, t, act, lane);
         }
         grid_barrier(A.barrier);
+        stamp(A, ts_k);
+        gc = -1;
         for (int item = gw; item < A.G * cblk; item += nw) {
             const int g = item / cblk;
-            const unsigned act = __ballot_sync(kFull, ld_cg(cprev + g * 32 + lane) != 0);
-            if (act) syncheck_item<Real>(A, g, item - g * cblk, t, act, lane);
+            if (g != gc) {
+                act = __ballot_sync(kFull, ld_cg(cprev + g * 32 + lane) != 0);
+                gc = g;
+            }
+            if (act) syncheck_item<Real, D>(A, g, item - g * cblk, t, act, lane);
         }
     }
 
@@ -436,13 +506,14 @@ decode_kernel(const DecodeArgs<Real> A)
     const int* cfin = A.cnt + (final_t & 1) * F;
     for (int f = gtid; f < A.B; f += nthreads) {
         const int c = ld_cg(cfin + f);
-        int it = A.iters[f];
+        const int it = A.iters[f];
         const bool conv = it >= 0;
         A.out_conv[f] = conv ? 1 : 0;
         A.out_iters[f] = conv ? it : A.max_it;
         A.out_mism[f] = conv ? 0 : c;
     }
     if (gtid == 0) *A.sweeps_run = final_t;
+    stamp(A, ts_k);
 }
 
 // ---------------------------------------------------------------------------
@@ -526,7 +597,7 @@ __global__ void words_to_rows_kernel(const unsigned* __restrict__ words, long lo
 
 // Alice side, Eq. 1: syndrome words of 32 frames per check, z = XOR of key
 // words over the row (syndrome_pass, _kernels.py:220-227, 32 frames wide).
-__global__ void syndrome_words_kernel(const int* __restrict__ chk_ptr, const int* __restrict__ chk_var,
+__global__ void syndrome_words_kernel(const uint8_t* __restrict__ deg, const int* __restrict__ chk_ell, int D,
                                       int n, int C, int G, const unsigned* __restrict__ key_w,
                                       unsigned* __restrict__ syn_w)
 {
@@ -535,8 +606,9 @@ __global__ void syndrome_words_kernel(const int* __restrict__ chk_ptr, const int
     for (long long it = (long long)blockIdx.x * blockDim.x + threadIdx.x; it < total; it += nth) {
         const int g = (int)(it / C), j = (int)(it % C);
         const unsigned* kw = key_w + (long long)g * n;
+        const int* row = chk_ell + (long long)j * D;
         unsigned p = 0;
-        for (int a = __ldg(chk_ptr + j); a < __ldg(chk_ptr + j + 1); ++a) p ^= __ldg(kw + __ldg(chk_var + a));
+        for (int k = 0, d = __ldg(deg + j); k < d; ++k) p ^= __ldg(kw + __ldg(row + k));
         syn_w[it] = p;
     }
 }
@@ -612,13 +684,14 @@ __global__ void posterior_phase_kernel(const int* __restrict__ var_ptr, const in
     post[i] = total;
 }
 
-// state readback: one frame's lane of an interleaved [..][32] array -> double
+// state readback: one frame's lane of an interleaved [..][32] array -> double,
+// optionally through an index map (reference edge id -> internal slot)
 template <class Real>
 __global__ void gather_lane_kernel(const Real* __restrict__ src, long long count, int lane,
-                                   double* __restrict__ dst)
+                                   const int* __restrict__ map, double* __restrict__ dst)
 {
     const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < count) dst[k] = (double)src[k * 32 + lane];
+    if (k < count) dst[k] = (double)src[(map ? (long long)map[k] : k) * 32 + lane];
 }
 
 }  // namespace mbp

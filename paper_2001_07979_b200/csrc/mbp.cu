@@ -86,10 +86,15 @@ struct mbp_ensemble {
     int n = 0, m = 0, u = 0, C = 0;
     long long E = 0;
     int dmax_c = 0, dmax_v = 0;
+    int D = 0;        // padded row stride of the ELL layout (kernel degree bound)
+    int dv_reg = 0;   // regular column degree (0 if irregular)
     int device = 0, sm_count = 0;
     float sat = 0.f;
-    std::vector<long long> edge_off;  // [u+1]
+    std::vector<long long> edge_off;  // [u+1] reference edge offsets
+    // reference CSR (single-phase kernels)
     DevBuf chk_ptr, chk_var, var_ptr, var_edge;  // int32
+    // decode layout: padded ELL rows + slot ids per variable
+    DevBuf deg, chk_ell, var_slot, ref2slot;
 };
 
 struct mbp_workspace {
@@ -98,7 +103,8 @@ struct mbp_workspace {
     int cap = 0, G = 0;
     size_t real_size = 4;
     DevBuf c2v, post, v2c, Lmag, noisy_w, syn_w, hard_w, hist_w, cnt, any_bad, iters, barrier,
-        sweeps, tmp_in, tmp_out, tmp_conv, tmp_iters, tmp_mism, tmp_e;
+        sweeps, ts, tmp_in, tmp_out, tmp_conv, tmp_iters, tmp_mism, tmp_e;
+    int ts_cap = 0;
     cudaStream_t own_stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
     int last_B = 0;
@@ -171,6 +177,23 @@ int mbp_ensemble_create(int32_t n, int32_t m, int32_t u, const int64_t* chk_ptr,
     ens->dmax_c = dmax_c;
     ens->dmax_v = dmax_v;
     ens->sat = saturation_threshold();
+    ens->D = pick_degree(std::max(dmax_c, 1));
+    ens->dv_reg = dmax_v;
+    for (int i = 0; i < n; ++i)
+        if (col_deg[i] != dmax_v) { ens->dv_reg = 0; break; }
+    // padded ELL: edge k of check j -> slot j*D + k (monotone in the reference edge id)
+    const int D = ens->D ? ens->D : 1;
+    std::vector<uint8_t> rowdeg(C);
+    std::vector<int> ell((size_t)C * D, 0), r2s(E), vs(E);
+    for (long long j = 0; j < C; ++j) {
+        const int d = (int)(chk_ptr[j + 1] - chk_ptr[j]);
+        rowdeg[j] = (uint8_t)std::min(d, 255);
+        for (int k = 0; k < d && k < D; ++k) {
+            ell[(size_t)j * D + k] = cv[chk_ptr[j] + k];
+            r2s[chk_ptr[j] + k] = (int)((size_t)j * D + k);
+        }
+    }
+    for (long long t = 0; t < E; ++t) vs[t] = r2s[ve[t]];
     int rc;
     {
         DeviceGuard dg(device);
@@ -182,7 +205,9 @@ int mbp_ensemble_create(int32_t n, int32_t m, int32_t u, const int64_t* chk_ptr,
         }
         ens->sm_count = prop.multiProcessorCount;
         if ((rc = ens->chk_ptr.alloc(sizeof(int) * (C + 1))) || (rc = ens->chk_var.alloc(sizeof(int) * E)) ||
-            (rc = ens->var_ptr.alloc(sizeof(int) * (n + 1))) || (rc = ens->var_edge.alloc(sizeof(int) * E))) {
+            (rc = ens->var_ptr.alloc(sizeof(int) * (n + 1))) || (rc = ens->var_edge.alloc(sizeof(int) * E)) ||
+            (rc = ens->deg.alloc(C)) || (rc = ens->chk_ell.alloc(sizeof(int) * (size_t)C * D)) ||
+            (rc = ens->var_slot.alloc(sizeof(int) * E)) || (rc = ens->ref2slot.alloc(sizeof(int) * E))) {
             delete ens;
             return rc;
         }
@@ -190,6 +215,10 @@ int mbp_ensemble_create(int32_t n, int32_t m, int32_t u, const int64_t* chk_ptr,
         if (err == cudaSuccess) err = cudaMemcpy(ens->chk_var.p, cv.data(), sizeof(int) * E, cudaMemcpyHostToDevice);
         if (err == cudaSuccess) err = cudaMemcpy(ens->var_ptr.p, vp.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice);
         if (err == cudaSuccess) err = cudaMemcpy(ens->var_edge.p, ve.data(), sizeof(int) * E, cudaMemcpyHostToDevice);
+        if (err == cudaSuccess) err = cudaMemcpy(ens->deg.p, rowdeg.data(), C, cudaMemcpyHostToDevice);
+        if (err == cudaSuccess) err = cudaMemcpy(ens->chk_ell.p, ell.data(), sizeof(int) * (size_t)C * D, cudaMemcpyHostToDevice);
+        if (err == cudaSuccess) err = cudaMemcpy(ens->var_slot.p, vs.data(), sizeof(int) * E, cudaMemcpyHostToDevice);
+        if (err == cudaSuccess) err = cudaMemcpy(ens->ref2slot.p, r2s.data(), sizeof(int) * E, cudaMemcpyHostToDevice);
         if (err != cudaSuccess) { delete ens; return fail(MBP_ECUDA, std::string("ensemble upload: ") + cudaGetErrorString(err)); }
     }
     *out = ens;
@@ -231,13 +260,16 @@ static int ws_alloc(mbp_workspace* ws)
     const size_t F = (size_t)ws->G * 32, R = ws->real_size;
     const size_t P = ws->cfg.combining_mode == MBP_ISOLATED_PER_MATRIX ? (size_t)ens->u + 1 : 1;
     int rc;
-    if (ws->c2v.bytes != ws->G * (size_t)ens->E * 32 * R && (rc = ws->c2v.alloc(ws->G * (size_t)ens->E * 32 * R))) return rc;
+    const size_t slots = (size_t)ens->C * ens->D;
+    if (ws->c2v.bytes != ws->G * slots * 32 * R && (rc = ws->c2v.alloc(ws->G * slots * 32 * R))) return rc;
     if (ws->post.bytes != ws->G * P * ens->n * 32 * R && (rc = ws->post.alloc(ws->G * P * ens->n * 32 * R))) return rc;
-    const size_t v2c_bytes = ws->cfg.damping != 0.0 ? ws->G * (size_t)ens->E * 32 * R : 0;
+    const size_t v2c_bytes = ws->cfg.damping != 0.0 ? ws->G * slots * 32 * R : 0;
     if (ws->v2c.bytes != v2c_bytes && (rc = ws->v2c.alloc(v2c_bytes))) return rc;
     const size_t hist_bytes = (ws->cfg.flags & MBP_RECORD_HISTORY)
         ? (size_t)(ws->cfg.max_iterations + 1) * ws->G * ens->n * 4 : 0;
     if (ws->hist_w.bytes != hist_bytes && (rc = ws->hist_w.alloc(hist_bytes))) return rc;
+    ws->ts_cap = (ws->cfg.flags & MBP_PROFILE_PHASES) ? 3 * (ws->cfg.max_iterations + 1) + 4 : 0;
+    if (ws->ts.bytes != (size_t)ws->ts_cap * 8 && (rc = ws->ts.alloc((size_t)ws->ts_cap * 8))) return rc;
     if (!ws->Lmag.p) {
         if ((rc = ws->Lmag.alloc(F * R)) || (rc = ws->noisy_w.alloc((size_t)ws->G * ens->n * 4)) ||
             (rc = ws->syn_w.alloc((size_t)ws->G * ens->C * 4)) || (rc = ws->hard_w.alloc((size_t)ws->G * ens->n * 4)) ||
@@ -352,7 +384,7 @@ static int dispatch_decode(mbp_workspace* ws, mbp::DecodeArgs<Real>& A, cudaStre
     if (damp) return launch_decode<Real, D, true, false>(ws, A, s);                  \
     if (iso) return launch_decode<Real, D, false, true>(ws, A, s);                   \
     return launch_decode<Real, D, false, false>(ws, A, s);
-    switch (pick_degree(ws->ens->dmax_c)) {
+    switch (ws->ens->D) {
     case 8: { MBP_DISPATCH_D(8) }
     case 16: { MBP_DISPATCH_D(16) }
     case 32: { MBP_DISPATCH_D(32) }
@@ -404,7 +436,7 @@ static int decode_chunk(mbp_workspace* ws, const uint8_t* noisy, const uint8_t* 
         fill_post_prior_kernel<Real><<<1024, 256, 0, s>>>(ws->noisy_w.as<unsigned>(), ws->Lmag.as<Real>(), G,
                                                           ens->n, P, ws->post.as<Real>());
         MBP_CUDA(cudaGetLastError());
-        MBP_CUDA(cudaMemsetAsync(ws->c2v.p, 0, (size_t)G * ens->E * 32 * sizeof(Real), s));
+        MBP_CUDA(cudaMemsetAsync(ws->c2v.p, 0, (size_t)G * ens->C * ens->D * 32 * sizeof(Real), s));
     }
     MBP_CUDA(cudaMemsetAsync(ws->cnt.p, 0, 2 * (size_t)F * 4, s));
     MBP_CUDA(cudaMemsetAsync(ws->any_bad.p, 0, 8, s));
@@ -413,10 +445,12 @@ static int decode_chunk(mbp_workspace* ws, const uint8_t* noisy, const uint8_t* 
 
     mbp::DecodeArgs<Real> A;
     std::memset(&A, 0, sizeof A);
-    A.n = ens->n; A.m = ens->m; A.u = ens->u; A.C = ens->C; A.E = (int)ens->E;
-    A.chk_ptr = ens->chk_ptr.as<int>(); A.chk_var = ens->chk_var.as<int>();
-    A.var_ptr = ens->var_ptr.as<int>(); A.var_edge = ens->var_edge.as<int>();
-    for (int l = 0; l <= ens->u; ++l) A.edge_off[l] = (int)ens->edge_off[l];
+    A.n = ens->n; A.m = ens->m; A.u = ens->u; A.C = ens->C;
+    A.slots = (long long)ens->C * ens->D;
+    A.deg = ens->deg.as<uint8_t>(); A.chk_ell = ens->chk_ell.as<int>();
+    A.var_ptr = ens->var_ptr.as<int>(); A.var_edge = ens->var_slot.as<int>();
+    A.dv = ens->dv_reg;
+    for (int l = 0; l <= ens->u; ++l) A.edge_off[l] = (long long)l * ens->m * ens->D;
     A.G = G;
     A.c2v = ws->c2v.as<Real>(); A.post = ws->post.as<Real>(); A.v2c = ws->v2c.as<Real>();
     A.Lmag = ws->Lmag.as<Real>();
@@ -424,6 +458,7 @@ static int decode_chunk(mbp_workspace* ws, const uint8_t* noisy, const uint8_t* 
     A.hard_w = ws->hard_w.as<unsigned>(); A.hist_w = record ? ws->hist_w.as<unsigned>() : nullptr;
     A.cnt = ws->cnt.as<int>(); A.any_bad = ws->any_bad.as<int>(); A.iters = ws->iters.as<int>();
     A.barrier = ws->barrier.as<unsigned>(); A.sweeps_run = ws->sweeps.as<int>();
+    A.ts = ws->ts_cap ? ws->ts.as<unsigned long long>() : nullptr; A.ts_cap = ws->ts_cap;
     A.B = B; A.out_conv = conv; A.out_iters = iters; A.out_mism = mism;
     A.max_it = cfg.max_iterations; A.clamp = (Real)cfg.llr_clamp; A.damping = (Real)cfg.damping;
     A.sat = ens->sat;
@@ -520,7 +555,7 @@ int mbp_syndrome_batch_device(mbp_workspace* ws, const uint8_t* keys, int64_t ba
             return rc;
         const long long items = (long long)G * ens->C;
         mbp::syndrome_words_kernel<<<(int)std::min<long long>((items + 255) / 256, 148LL * 32), 256, 0, s>>>(
-            ens->chk_ptr.as<int>(), ens->chk_var.as<int>(), ens->n, ens->C, G, ws->noisy_w.as<unsigned>(),
+            ens->deg.as<uint8_t>(), ens->chk_ell.as<int>(), ens->D, ens->n, ens->C, G, ws->noisy_w.as<unsigned>(),
             ws->syn_w.as<unsigned>());
         MBP_CUDA(cudaGetLastError());
         if ((rc = launch_words_to_rows(ws->syn_w.as<unsigned>(), ens->C, B, G, ens->u, ens->m, mb,
@@ -551,16 +586,17 @@ int mbp_syndrome_batch(mbp_workspace* ws, const uint8_t* keys, int64_t batch, ui
 // ---------------------------------------------------------------------------
 // state readback
 // ---------------------------------------------------------------------------
-static int read_lane(mbp_workspace* ws, const void* base, long long count, int64_t frame, double* out)
+static int read_lane(mbp_workspace* ws, const void* base, long long count, int64_t frame, double* out,
+                     const int* map = nullptr)
 {
     DevBuf tmp;
     int rc;
     if ((rc = tmp.alloc(count * 8))) return rc;
     const int lane = (int)(frame & 31);
     if (ws->real_size == 8)
-        mbp::gather_lane_kernel<double><<<(int)((count + 255) / 256), 256>>>((const double*)base, count, lane, tmp.as<double>());
+        mbp::gather_lane_kernel<double><<<(int)((count + 255) / 256), 256>>>((const double*)base, count, lane, map, tmp.as<double>());
     else
-        mbp::gather_lane_kernel<float><<<(int)((count + 255) / 256), 256>>>((const float*)base, count, lane, tmp.as<double>());
+        mbp::gather_lane_kernel<float><<<(int)((count + 255) / 256), 256>>>((const float*)base, count, lane, map, tmp.as<double>());
     MBP_CUDA(cudaGetLastError());
     MBP_CUDA(cudaMemcpy(out, tmp.p, count * 8, cudaMemcpyDeviceToHost));
     return MBP_OK;
@@ -589,8 +625,8 @@ int mbp_workspace_read_c2v(mbp_workspace* ws, int64_t frame, double* c2v)
     const mbp_ensemble* ens = ws->ens;
     DeviceGuard dg(ens->device);
     MBP_CUDA(cudaDeviceSynchronize());
-    const char* base = ws->c2v.as<char>() + ((size_t)(frame / 32) * ens->E * 32) * ws->real_size;
-    return read_lane(ws, base, ens->E, frame, c2v);
+    const char* base = ws->c2v.as<char>() + ((size_t)(frame / 32) * ens->C * ens->D * 32) * ws->real_size;
+    return read_lane(ws, base, ens->E, frame, c2v, ens->ref2slot.as<int>());
 }
 
 int mbp_workspace_read_v2c(mbp_workspace* ws, int64_t frame, double* v2c)
@@ -601,8 +637,8 @@ int mbp_workspace_read_v2c(mbp_workspace* ws, int64_t frame, double* v2c)
     const mbp_ensemble* ens = ws->ens;
     DeviceGuard dg(ens->device);
     MBP_CUDA(cudaDeviceSynchronize());
-    const char* base = ws->v2c.as<char>() + ((size_t)(frame / 32) * ens->E * 32) * ws->real_size;
-    return read_lane(ws, base, ens->E, frame, v2c);
+    const char* base = ws->v2c.as<char>() + ((size_t)(frame / 32) * ens->C * ens->D * 32) * ws->real_size;
+    return read_lane(ws, base, ens->E, frame, v2c, ens->ref2slot.as<int>());
 }
 
 int mbp_workspace_read_history(mbp_workspace* ws, int64_t frame, int32_t rows, uint8_t* out)
@@ -624,6 +660,21 @@ int mbp_workspace_read_history(mbp_workspace* ws, int64_t frame, int32_t rows, u
         std::memset(r, 0, nb);
         for (size_t i = 0; i < n; ++i) r[i >> 3] |= (uint8_t)(((w[i] >> lane) & 1u) << (i & 7));
     }
+    return MBP_OK;
+}
+
+int mbp_workspace_read_phase_times(mbp_workspace* ws, uint64_t* ns, int32_t cap, int32_t* count)
+{
+    if (!ws || !ns || !count) return fail(MBP_EINVAL, "null pointer argument");
+    if (!ws->ts_cap) return fail(MBP_EINVAL, "workspace was not configured with MBP_PROFILE_PHASES");
+    DeviceGuard dg(ws->ens->device);
+    MBP_CUDA(cudaDeviceSynchronize());
+    int sweeps = 0;
+    MBP_CUDA(cudaMemcpy(&sweeps, ws->sweeps.p, 4, cudaMemcpyDeviceToHost));
+    // stamps: start, 3 per executed sweep, the final check's barrier, end
+    const int k = std::min(ws->ts_cap, 3 * sweeps + 3);
+    *count = k;
+    MBP_CUDA(cudaMemcpy(ns, ws->ts.p, (size_t)std::min(k, cap) * 8, cudaMemcpyDeviceToHost));
     return MBP_OK;
 }
 

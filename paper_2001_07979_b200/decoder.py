@@ -288,6 +288,24 @@ class BatchDecoder:
         N.call("mbp_workspace_read_history", self.handle, int(k), int(rows), out.ctypes.data)
         return np.unpackbits(out, axis=1, count=self.dev.n, bitorder="little")
 
+    def phase_times(self) -> dict:
+        """Per-phase device time (ms) of the last decode chunk
+        (needs flags MBP_PROFILE_PHASES): check / variable / syndrome phase
+        totals over the executed sweeps, the initial check and the tail."""
+        cap = 3 * (self.config.max_iterations + 1) + 4
+        buf = np.zeros(cap, dtype=np.uint64)
+        cnt = C.c_int32(0)
+        N.call("mbp_workspace_read_phase_times", self.handle, buf.ctypes.data, cap, C.byref(cnt))
+        ts = buf[: min(cnt.value, cap)].astype(np.float64) / 1e6
+        d = np.diff(ts)
+        sweeps = (len(ts) - 3) // 3
+        out = {"sweeps": sweeps, "total_ms": float(ts[-1] - ts[0]), "syncheck0_ms": float(d[0])}
+        if sweeps:
+            body = d[1:1 + 3 * sweeps].reshape(sweeps, 3)
+            out.update(check_ms=body[:, 0].tolist(), var_ms=body[:, 1].tolist(), syncheck_ms=body[:, 2].tolist())
+        out["tail_ms"] = float(d[-1]) if len(d) > 1 else 0.0
+        return out
+
     def last_timing(self, e2e: bool = False):
         """(decode-kernel ms, sweeps run) of the last decode; with e2e=True
         also the device-timed ms of the last host-buffer call."""
