@@ -35,11 +35,38 @@ constexpr int kMaxU = 16;
 template <class T> __device__ __forceinline__ T ld_cg(const T* p) { return __ldcg(p); }
 template <class T> __device__ __forceinline__ T ld_ro(const T* p) { return __ldg(p); }
 
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p)
+// relaxed (no L1 invalidation per poll, unlike ld.acquire which emits CCTL.IVALL)
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p)
 {
     unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+
+// predicated loads/stores without branches (uniform or per-lane predicate)
+__device__ __forceinline__ float ld_cg_if(const float* p, bool pred)
+{
+    float v = 0.0f;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.cg.f32 %0, [%1];\n\t}"
+                 : "+f"(v) : "l"(p), "r"((int)pred) : "memory");
+    return v;
+}
+__device__ __forceinline__ double ld_cg_if(const double* p, bool pred)
+{
+    double v = 0.0;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.cg.f64 %0, [%1];\n\t}"
+                 : "+d"(v) : "l"(p), "r"((int)pred) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_if(float* p, float v, bool pred)
+{
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.f32 [%0], %1;\n\t}"
+                 :: "l"(p), "f"(v), "r"((int)pred) : "memory");
+}
+__device__ __forceinline__ void st_if(double* p, double v, bool pred)
+{
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.f64 [%0], %1;\n\t}"
+                 :: "l"(p), "d"(v), "r"((int)pred) : "memory");
 }
 
 // Grid-wide barrier for a cooperatively launched (co-resident) grid.
@@ -48,14 +75,14 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar)
 {
     __syncthreads();
     if (threadIdx.x == 0) {
-        const unsigned gen = ld_acquire(bar + 1);
+        const unsigned gen = ld_relaxed(bar + 1);
         __threadfence();
         if (atomicAdd(bar, 1u) == gridDim.x - 1) {
             bar[0] = 0;
             __threadfence();
             atomicAdd(bar + 1, 1u);
         } else {
-            while (ld_acquire(bar + 1) == gen) __nanosleep(20);
+            while (ld_relaxed(bar + 1) == gen) __nanosleep(32);
         }
         __threadfence();
     }
@@ -103,8 +130,9 @@ __device__ __forceinline__ float phi_f32(float x)
     return t < 0.125f ? ser : L;
 }
 
-template <int D> struct SignMask { using T = unsigned; };
-template <> struct SignMask<64> { using T = unsigned long long; };
+template <bool Wide> struct SignMaskT { using T = unsigned; };
+template <> struct SignMaskT<true> { using T = unsigned long long; };
+template <int D> struct SignMask { using T = typename SignMaskT<(D > 32)>::T; };
 
 template <int D>
 __device__ __forceinline__ void c2v_rule(const float (&x)[D], int d, unsigned flip, float clamp,
@@ -115,12 +143,10 @@ __device__ __forceinline__ void c2v_rule(const float (&x)[D], int d, unsigned fl
     M sg = 0;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-        ph[k] = 0.0f;
-        if (k < d) {
-            const float a = fabsf(x[k]);
-            ph[k] = a >= sat ? 0.0f : phi_f32(a);
-            sg |= (M)(x[k] < 0.0f) << k;
-        }
+        const float a = fabsf(x[k]);
+        const float f = phi_f32(a);
+        ph[k] = (k < d && a < sat) ? f : 0.0f;   // padding slots contribute nothing
+        sg |= (M)(x[k] < 0.0f) << k;             // padding x == 0: sign bit 0
     }
     float suf[D];
     float s = 0.0f;
@@ -133,13 +159,11 @@ __device__ __forceinline__ void c2v_rule(const float (&x)[D], int d, unsigned fl
     float pre = 0.0f;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-        if (k < d) {
-            const float ex = pre + suf[k];
-            pre += ph[k];
-            const float mag = fminf(phi_f32(ex), clamp);
-            const unsigned neg = par ^ (unsigned)((sg >> k) & 1) ^ flip;
-            out[k] = neg ? -mag : mag;
-        }
+        const float ex = pre + suf[k];
+        pre += ph[k];
+        const float mag = fminf(phi_f32(ex), clamp);
+        const unsigned neg = par ^ (unsigned)((sg >> k) & 1) ^ flip;
+        out[k] = neg ? -mag : mag;
     }
 }
 
@@ -189,9 +213,10 @@ template <class Real>
 struct DecodeArgs {
     // graph
     int n, m, u, C;
-    long long slots;                   // C * D
+    int Ds;                            // ELL row stride (= max check degree)
+    long long slots;                   // C * Ds
     const uint8_t* __restrict__ deg;   // [C] row degree
-    const int* __restrict__ chk_ell;   // [C*D] var ids (pad 0)
+    const int* __restrict__ chk_ell;   // [C*Ds] var ids (pad 0)
     const int* __restrict__ var_ptr;   // [n+1] into var_edge (CSR; unused when dv > 0)
     const int* __restrict__ var_edge;  // [E] slot ids, ascending per variable
     int dv;                            // regular column degree, 0 if irregular
@@ -211,6 +236,7 @@ struct DecodeArgs {
     int* __restrict__ any_bad;   // [2]
     int* __restrict__ iters;     // [G*32] first converged sweep, -1 unset
     unsigned* __restrict__ barrier;  // [2]
+    unsigned* __restrict__ work;     // [3*(T+1)+1] dynamic work counters, zeroed per launch
     int* __restrict__ sweeps_run;    // [1]
     unsigned long long* __restrict__ ts;  // phase timestamps (globaltimer ns) or null
     int ts_cap;
@@ -227,22 +253,25 @@ struct DecodeArgs {
 };
 
 // Check phase item: check j of group g at sweep t; `act` = lanes (frames)
-// still decoding.  Reads post_{t-1}, c2v_{t-1}, writes c2v_t.
+// still decoding.  Reads post_{t-1}, c2v_{t-1}, writes c2v_t.  Branch-free
+// over the D slots (D = the launch's degree bound): slots k >= d(j) are
+// predicated off, so the only divergence is none.
 template <class Real, int D, bool DAMP, bool ISO>
 __device__ __forceinline__ void check_item(const DecodeArgs<Real>& A, int g, int j, int t,
                                            unsigned act, int lane)
 {
     const int d = ld_ro(A.deg + j);
     constexpr int NC = (D + 31) / 32;
+    const int* row = A.chk_ell + j * A.Ds;
     int vid[NC];
 #pragma unroll
-    for (int c = 0; c < NC; ++c)
-        vid[c] = (c * 32 + lane < D) ? ld_ro(A.chk_ell + (size_t)j * D + c * 32 + lane) : 0;
+    for (int c = 0; c < NC; ++c) vid[c] = (c * 32 + lane < d) ? ld_ro(row + c * 32 + lane) : 0;
     const bool live = (act >> lane) & 1u;
     const unsigned flip = (ld_ro(A.syn_w + (size_t)g * A.C + j) >> lane) & 1u;
     const Real L = ld_ro(A.Lmag + g * 32 + lane);
     const int mat = ISO ? j / A.m : 0;
-    const size_t line0 = ((size_t)g * A.slots + (size_t)j * D) * 32 + lane;
+    Real* c2v_row = A.c2v + ((size_t)g * A.slots + (size_t)j * A.Ds) * 32 + lane;
+    Real* v2c_row = DAMP ? A.v2c + ((size_t)g * A.slots + (size_t)j * A.Ds) * 32 + lane : nullptr;
     const Real* postg = A.post + ((size_t)g * (ISO ? A.u + 1 : 1) + mat) * A.n * 32 + lane;
 
     Real x[D];
@@ -251,61 +280,90 @@ __device__ __forceinline__ void check_item(const DecodeArgs<Real>& A, int g, int
         const unsigned* nw = A.noisy_w + (size_t)g * A.n;
 #pragma unroll
         for (int k = 0; k < D; ++k) {
-            x[k] = Real(0);
-            if (k < d) {
-                const int v = __shfl_sync(kFull, vid[k >> 5], k & 31);
-                x[k] = ((ld_ro(nw + v) >> lane) & 1u) ? -L : L;
-            }
+            const int v = __shfl_sync(kFull, vid[k >> 5], k & 31);
+            const unsigned w = k < d ? ld_ro(nw + v) : 0u;
+            x[k] = k < d ? (((w >> lane) & 1u) ? -L : L) : Real(0);
         }
-        if (DAMP && live) {
+        if (DAMP) {
 #pragma unroll
-            for (int k = 0; k < D; ++k)
-                if (k < d) A.v2c[line0 + (size_t)k * 32] = x[k];
+            for (int k = 0; k < D; ++k) st_if(v2c_row + k * 32, x[k], live && k < d);
         }
     } else {
         Real p[D], q[D];
 #pragma unroll
         for (int k = 0; k < D; ++k) {
-            p[k] = Real(0);
-            q[k] = Real(0);
-            if (k < d) {
-                const int v = __shfl_sync(kFull, vid[k >> 5], k & 31);
-                if (live) {
-                    p[k] = ld_cg(postg + (size_t)v * 32);
-                    q[k] = ld_cg(A.c2v + line0 + (size_t)k * 32);
-                }
-            }
+            const int v = __shfl_sync(kFull, vid[k >> 5], k & 31);
+            const bool pk = live && k < d;
+            p[k] = ld_cg_if(postg + (unsigned)v * 32u, pk);
+            q[k] = ld_cg_if(c2v_row + k * 32, pk);
         }
+        if (DAMP) {
 #pragma unroll
-        for (int k = 0; k < D; ++k) {
-            Real val = p[k] - q[k];
-            if (DAMP) {
-                if (k < d && live) {
-                    const Real old = ld_cg(A.v2c + line0 + (size_t)k * 32);
-                    val = (Real(1) - A.damping) * val + A.damping * old;
-                }
+            for (int k = 0; k < D; ++k) {
+                const Real old = ld_cg_if(v2c_row + k * 32, live && k < d);
+                x[k] = clampr((Real(1) - A.damping) * (p[k] - q[k]) + A.damping * old, A.clamp);
+                st_if(v2c_row + k * 32, x[k], live && k < d);
             }
-            x[k] = clampr(val, A.clamp);
-        }
-        if (DAMP && live) {
+        } else {
 #pragma unroll
-            for (int k = 0; k < D; ++k)
-                if (k < d) A.v2c[line0 + (size_t)k * 32] = x[k];
+            for (int k = 0; k < D; ++k) x[k] = clampr(p[k] - q[k], A.clamp);
         }
     }
     Real out[D];
     c2v_rule<D>(x, d, flip, A.clamp, A.sat, out);
-    if (live) {
 #pragma unroll
-        for (int k = 0; k < D; ++k)
-            if (k < d) A.c2v[line0 + (size_t)k * 32] = out[k];
+    for (int k = 0; k < D; ++k) st_if(c2v_row + k * 32, out[k], live && k < d);
+}
+
+// Variable phase, regular column degree DV, NV variables per warp pass
+// (independent load streams in flight): joint posterior prior + sum of every
+// matrix's c2v in ascending edge order (posterior_pass, _kernels.py:293-301),
+// hard decision post < 0 (ties -> 0) as a ballot (hard_pass).
+template <class Real, int DV, int NV>
+__device__ __forceinline__ void var_items_regular(const DecodeArgs<Real>& A, int g, int i0, int nv, int t,
+                                                  unsigned act, int lane)
+{
+    const bool live = (act >> lane) & 1u;
+    const Real* c2vg = A.c2v + (size_t)g * A.slots * 32 + lane;
+    const Real L = ld_ro(A.Lmag + g * 32 + lane);
+    int eid[NV];
+    unsigned nwd[NV], old[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        const int i = i0 + v;
+        const bool ok = v < nv;
+        eid[v] = (ok && lane < DV) ? ld_ro(A.var_edge + i * DV + lane) : 0;
+        nwd[v] = ok ? ld_ro(A.noisy_w + (size_t)g * A.n + i) : 0u;
+        old[v] = (ok && lane == 0) ? ld_cg(A.hard_w + (size_t)g * A.n + i) : 0u;
+    }
+    Real c[NV][DV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int k = 0; k < DV; ++k) {
+            const int e = __shfl_sync(kFull, eid[v], k);
+            c[v][k] = ld_cg_if(c2vg + (unsigned)e * 32u, live && v < nv);
+        }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        if (v >= nv) break;
+        const int i = i0 + v;
+        Real acc = ((nwd[v] >> lane) & 1u) ? -L : L;
+#pragma unroll
+        for (int k = 0; k < DV; ++k) acc += c[v][k];
+        const size_t w = (size_t)g * A.n + i;
+        st_if(A.post + w * 32 + lane, acc, live);
+        const unsigned neg = __ballot_sync(kFull, acc < Real(0));
+        if (lane == 0) {
+            const unsigned hw = (neg & act) | (old[v] & ~act);
+            A.hard_w[w] = hw;
+            if (A.hist_w) A.hist_w[((size_t)t * A.G) * A.n + w] = hw;
+        }
     }
 }
 
-// Variable phase item: variable i of group g at sweep t.  Joint posterior
-// prior + sum of every matrix's c2v in ascending edge order (posterior_pass);
-// in isolated mode also the per-matrix totals v2c_pass uses
-// (_kernels.py:276-279).  Hard decision post < 0 (ties -> 0) as a ballot.
+// Variable phase, general degrees (CSR) and isolated-per-matrix mode: also
+// the per-matrix totals v2c_pass uses (_kernels.py:276-279).
 template <class Real, bool ISO>
 __device__ __forceinline__ void var_item(const DecodeArgs<Real>& A, int g, int i, int t,
                                          unsigned act, int lane)
@@ -324,33 +382,13 @@ __device__ __forceinline__ void var_item(const DecodeArgs<Real>& A, int g, int i
         for (int base = 0; base < dv; base += 32) {
             const int eid = base + lane < dv ? ld_ro(A.var_edge + p0 + base + lane) : 0;
             const int cnt = min(32, dv - base);
-            if (cnt == 6) {  // regular column degree 3 at u = 2: fully unrolled
-                Real c[6];
-#pragma unroll
-                for (int k = 0; k < 6; ++k) {
-                    const int e = __shfl_sync(kFull, eid, k);
-                    c[k] = live ? ld_cg(c2vg + (size_t)e * 32) : Real(0);
-                }
-#pragma unroll
-                for (int k = 0; k < 6; ++k) acc += c[k];
-            } else if (cnt == 9) {  // u = 3
-                Real c[9];
-#pragma unroll
-                for (int k = 0; k < 9; ++k) {
-                    const int e = __shfl_sync(kFull, eid, k);
-                    c[k] = live ? ld_cg(c2vg + (size_t)e * 32) : Real(0);
-                }
-#pragma unroll
-                for (int k = 0; k < 9; ++k) acc += c[k];
-            } else {
 #pragma unroll 4
-                for (int k = 0; k < cnt; ++k) {
-                    const int e = __shfl_sync(kFull, eid, k);
-                    if (live) acc += ld_cg(c2vg + (size_t)e * 32);
-                }
+            for (int k = 0; k < cnt; ++k) {
+                const int e = __shfl_sync(kFull, eid, k);
+                acc += ld_cg_if(c2vg + (size_t)e * 32, live);
             }
         }
-        if (live) A.post[w * 32 + lane] = acc;
+        st_if(A.post + w * 32 + lane, acc, live);
     } else {
         const size_t P = (size_t)(A.u + 1);
         Real part = prior;
@@ -361,20 +399,20 @@ __device__ __forceinline__ void var_item(const DecodeArgs<Real>& A, int g, int i
             for (int k = 0; k < cnt; ++k) {
                 const int e = __shfl_sync(kFull, eid, k);
                 while (e >= A.edge_off[l + 1]) {  // close the totals of matrices before e's
-                    if (live) A.post[(((size_t)g * P + l) * A.n + i) * 32 + lane] = part;
+                    st_if(A.post + (((size_t)g * P + l) * A.n + i) * 32 + lane, part, live);
                     part = prior;
                     ++l;
                 }
-                const Real c = live ? ld_cg(c2vg + (size_t)e * 32) : Real(0);
-                acc += c;
-                part += c;
+                const Real cv = ld_cg_if(c2vg + (size_t)e * 32, live);
+                acc += cv;
+                part += cv;
             }
         }
         for (; l < A.u; ++l) {
-            if (live) A.post[(((size_t)g * P + l) * A.n + i) * 32 + lane] = part;
+            st_if(A.post + (((size_t)g * P + l) * A.n + i) * 32 + lane, part, live);
             part = prior;
         }
-        if (live) A.post[(((size_t)g * P + A.u) * A.n + i) * 32 + lane] = acc;
+        st_if(A.post + (((size_t)g * P + A.u) * A.n + i) * 32 + lane, acc, live);
     }
     const unsigned neg = __ballot_sync(kFull, acc < Real(0));
     if (lane == 0) {
@@ -387,7 +425,7 @@ __device__ __forceinline__ void var_item(const DecodeArgs<Real>& A, int g, int i
 // Syndrome phase item: 32 consecutive checks (lane = check) of group g.
 // Mismatch words (bit f = frame f) are turned into per-frame counts with 32
 // ballots and added to cnt[t&1].
-template <class Real, int D>
+template <class Real>
 __device__ __forceinline__ void syncheck_item(const DecodeArgs<Real>& A, int g, int blk, int t,
                                               unsigned act, int lane)
 {
@@ -396,7 +434,7 @@ __device__ __forceinline__ void syncheck_item(const DecodeArgs<Real>& A, int g, 
     if (j < A.C) {
         const unsigned* hw = A.hard_w + (size_t)g * A.n;
         const int d = ld_ro(A.deg + j);
-        const int* row = A.chk_ell + (size_t)j * D;
+        const int* row = A.chk_ell + j * A.Ds;
         unsigned par = 0;
         for (int k = 0; k < d; ++k) par ^= ld_cg(hw + ld_ro(row + k));
         mism = (par ^ ld_ro(A.syn_w + (size_t)g * A.C + j)) & act;
@@ -425,6 +463,23 @@ __device__ __forceinline__ void stamp(const DecodeArgs<Real>& A, int& k)
     ++k;
 }
 
+// Dynamic work distribution: warps claim chunks of kChunk consecutive items
+// from a per-phase counter (balanced tails; consecutive items stay in one
+// group so the group's active mask is loaded once per chunk).
+constexpr int kChunk = 16;
+
+__device__ __forceinline__ int claim(unsigned* counter, int lane)
+{
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(counter, (unsigned)kChunk);
+    return (int)__shfl_sync(kFull, base, 0);
+}
+
+__device__ __forceinline__ unsigned group_mask(const int* cprev, int g, int lane)
+{
+    return __ballot_sync(kFull, ld_cg(cprev + g * 32 + lane) != 0);
+}
+
 template <class Real, int D>
 constexpr int decode_min_blocks() { return (sizeof(Real) == 4 && D <= 16) ? 4 : 2; }
 
@@ -435,19 +490,22 @@ __global__ void __launch_bounds__(kDecodeThreads, decode_min_blocks<Real, D>())
 decode_kernel(const DecodeArgs<Real> A)
 {
     const int lane = threadIdx.x & 31;
-    const int warps_per_block = blockDim.x >> 5;
-    const int gw = blockIdx.x * warps_per_block + (threadIdx.x >> 5);
-    const int nw = gridDim.x * warps_per_block;
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const int nthreads = gridDim.x * blockDim.x;
     const int F = A.G * 32;
     const int cblk = (A.C + 31) / 32;
     int ts_k = 0;
+    int wc = 0;  // next work counter
     stamp(A, ts_k);
 
     // iteration 0: the uncorrected key against all u*m syndromes (_kernels.py:358-365)
-    for (int item = gw; item < A.G * cblk; item += nw)
-        syncheck_item<Real, D>(A, item / cblk, item % cblk, 0, kFull, lane);
+    {
+        const int total = A.G * cblk;
+        for (int base = claim(A.work + wc, lane); base < total; base = claim(A.work + wc, lane))
+            for (int item = base; item < min(base + kChunk, total); ++item)
+                syncheck_item<Real>(A, item / cblk, item % cblk, 0, kFull, lane);
+        ++wc;
+    }
 
     int t = 1;
     int final_t = 0;
@@ -466,39 +524,63 @@ decode_kernel(const DecodeArgs<Real> A)
         }
         if (gtid == 0) A.any_bad[t & 1] = 0;
 
-        // the active-frame mask of a group is cached per warp: grid-stride
-        // items of a warp stay in one group for many consecutive items
-        int gc = -1;
-        unsigned act = 0;
-        for (int item = gw; item < A.G * A.C; item += nw) {
-            const int g = item / A.C;
-            if (g != gc) {
-                act = __ballot_sync(kFull, ld_cg(cprev + g * 32 + lane) != 0);
-                gc = g;
+        {   // check phase
+            const int total = A.G * A.C;
+            for (int base = claim(A.work + wc, lane); base < total; base = claim(A.work + wc, lane)) {
+                const int end = min(base + kChunk, total);
+                int g = base / A.C;
+                unsigned act = group_mask(cprev, g, lane);
+                for (int item = base; item < end; ++item) {
+                    const int gi = item / A.C;
+                    if (gi != g) { g = gi; act = group_mask(cprev, g, lane); }
+                    if (act) check_item<Real, D, DAMP, ISO>(A, g, item - g * A.C, t, act, lane);
+                }
             }
-            if (act) check_item<Real, D, DAMP, ISO>(A, g, item - g * A.C, t, act, lane);
+            ++wc;
         }
         grid_barrier(A.barrier);
         stamp(A, ts_k);
-        gc = -1;
-        for (int item = gw; item < A.G * A.n; item += nw) {
-            const int g = item / A.n;
-            if (g != gc) {
-                act = __ballot_sync(kFull, ld_cg(cprev + g * 32 + lane) != 0);
-                gc = g;
+        {   // variable phase
+            const int total = A.G * A.n;
+            for (int base = claim(A.work + wc, lane); base < total; base = claim(A.work + wc, lane)) {
+                const int end = min(base + kChunk, total);
+                int item = base;
+                while (item < end) {
+                    const int g = item / A.n;
+                    const int i = item - g * A.n;
+                    const unsigned act = group_mask(cprev, g, lane);
+                    const int span = min(end - item, A.n - i);  // items left in this group
+                    if (act) {
+                        if (!ISO && A.dv == 6) {
+                            for (int k = 0; k < span; k += 2)
+                                var_items_regular<Real, 6, 2>(A, g, i + k, min(2, span - k), t, act, lane);
+                        } else if (!ISO && A.dv == 9) {
+                            for (int k = 0; k < span; k += 2)
+                                var_items_regular<Real, 9, 2>(A, g, i + k, min(2, span - k), t, act, lane);
+                        } else {
+                            for (int k = 0; k < span; ++k) var_item<Real, ISO>(A, g, i + k, t, act, lane);
+                        }
+                    }
+                    item += span;
+                }
             }
-            if (act) var_item<Real, ISO>(A, g, item - g * A.n, t, act, lane);
+            ++wc;
         }
         grid_barrier(A.barrier);
         stamp(A, ts_k);
-        gc = -1;
-        for (int item = gw; item < A.G * cblk; item += nw) {
-            const int g = item / cblk;
-            if (g != gc) {
-                act = __ballot_sync(kFull, ld_cg(cprev + g * 32 + lane) != 0);
-                gc = g;
+        {   // syndrome phase
+            const int total = A.G * cblk;
+            for (int base = claim(A.work + wc, lane); base < total; base = claim(A.work + wc, lane)) {
+                const int end = min(base + kChunk, total);
+                int g = base / cblk;
+                unsigned act = group_mask(cprev, g, lane);
+                for (int item = base; item < end; ++item) {
+                    const int gi = item / cblk;
+                    if (gi != g) { g = gi; act = group_mask(cprev, g, lane); }
+                    if (act) syncheck_item<Real>(A, g, item - g * cblk, t, act, lane);
+                }
             }
-            if (act) syncheck_item<Real, D>(A, g, item - g * cblk, t, act, lane);
+            ++wc;
         }
     }
 

@@ -86,7 +86,7 @@ struct mbp_ensemble {
     int n = 0, m = 0, u = 0, C = 0;
     long long E = 0;
     int dmax_c = 0, dmax_v = 0;
-    int D = 0;        // padded row stride of the ELL layout (kernel degree bound)
+    int Ds = 0;       // ELL row stride = max check degree
     int dv_reg = 0;   // regular column degree (0 if irregular)
     int device = 0, sm_count = 0;
     float sat = 0.f;
@@ -103,7 +103,7 @@ struct mbp_workspace {
     int cap = 0, G = 0;
     size_t real_size = 4;
     DevBuf c2v, post, v2c, Lmag, noisy_w, syn_w, hard_w, hist_w, cnt, any_bad, iters, barrier,
-        sweeps, ts, tmp_in, tmp_out, tmp_conv, tmp_iters, tmp_mism, tmp_e;
+        sweeps, ts, work, tmp_in, tmp_out, tmp_conv, tmp_iters, tmp_mism, tmp_e;
     int ts_cap = 0;
     cudaStream_t own_stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
@@ -177,12 +177,12 @@ int mbp_ensemble_create(int32_t n, int32_t m, int32_t u, const int64_t* chk_ptr,
     ens->dmax_c = dmax_c;
     ens->dmax_v = dmax_v;
     ens->sat = saturation_threshold();
-    ens->D = pick_degree(std::max(dmax_c, 1));
+    ens->Ds = std::max(dmax_c, 1);
     ens->dv_reg = dmax_v;
     for (int i = 0; i < n; ++i)
         if (col_deg[i] != dmax_v) { ens->dv_reg = 0; break; }
-    // padded ELL: edge k of check j -> slot j*D + k (monotone in the reference edge id)
-    const int D = ens->D ? ens->D : 1;
+    // padded ELL: edge k of check j -> slot j*Ds + k (monotone in the reference edge id)
+    const int D = ens->Ds;
     std::vector<uint8_t> rowdeg(C);
     std::vector<int> ell((size_t)C * D, 0), r2s(E), vs(E);
     for (long long j = 0; j < C; ++j) {
@@ -260,7 +260,7 @@ static int ws_alloc(mbp_workspace* ws)
     const size_t F = (size_t)ws->G * 32, R = ws->real_size;
     const size_t P = ws->cfg.combining_mode == MBP_ISOLATED_PER_MATRIX ? (size_t)ens->u + 1 : 1;
     int rc;
-    const size_t slots = (size_t)ens->C * ens->D;
+    const size_t slots = (size_t)ens->C * ens->Ds;
     if (ws->c2v.bytes != ws->G * slots * 32 * R && (rc = ws->c2v.alloc(ws->G * slots * 32 * R))) return rc;
     if (ws->post.bytes != ws->G * P * ens->n * 32 * R && (rc = ws->post.alloc(ws->G * P * ens->n * 32 * R))) return rc;
     const size_t v2c_bytes = ws->cfg.damping != 0.0 ? ws->G * slots * 32 * R : 0;
@@ -268,6 +268,8 @@ static int ws_alloc(mbp_workspace* ws)
     const size_t hist_bytes = (ws->cfg.flags & MBP_RECORD_HISTORY)
         ? (size_t)(ws->cfg.max_iterations + 1) * ws->G * ens->n * 4 : 0;
     if (ws->hist_w.bytes != hist_bytes && (rc = ws->hist_w.alloc(hist_bytes))) return rc;
+    const size_t work_bytes = (size_t)(3 * (ws->cfg.max_iterations + 1) + 2) * 4;
+    if (ws->work.bytes != work_bytes && (rc = ws->work.alloc(work_bytes))) return rc;
     ws->ts_cap = (ws->cfg.flags & MBP_PROFILE_PHASES) ? 3 * (ws->cfg.max_iterations + 1) + 4 : 0;
     if (ws->ts.bytes != (size_t)ws->ts_cap * 8 && (rc = ws->ts.alloc((size_t)ws->ts_cap * 8))) return rc;
     if (!ws->Lmag.p) {
@@ -374,24 +376,53 @@ static int launch_decode(mbp_workspace* ws, mbp::DecodeArgs<Real>& A, cudaStream
     return MBP_OK;
 }
 
-template <class Real>
-static int dispatch_decode(mbp_workspace* ws, mbp::DecodeArgs<Real>& A, cudaStream_t s)
+// Degree bound of the launch: the production variant (fp32, joint, no
+// damping) is instantiated for every exact max row degree up to 16 (no
+// padded compute), the others for powers of two.
+static int kernel_degree(int Ds, bool fast)
+{
+    if (fast) {
+        if (Ds <= 16) return std::max(Ds, 3);
+        for (int d : {20, 24, 28, 32, 48, 64}) if (Ds <= d) return d;
+        return 0;
+    }
+    return pick_degree(Ds);
+}
+
+template <class Real, int D>
+static int launch_variant(mbp_workspace* ws, mbp::DecodeArgs<Real>& A, cudaStream_t s)
 {
     const bool damp = ws->cfg.damping != 0.0;
     const bool iso = ws->cfg.combining_mode == MBP_ISOLATED_PER_MATRIX;
-#define MBP_DISPATCH_D(D)                                                            \
-    if (damp && iso) return launch_decode<Real, D, true, true>(ws, A, s);            \
-    if (damp) return launch_decode<Real, D, true, false>(ws, A, s);                  \
-    if (iso) return launch_decode<Real, D, false, true>(ws, A, s);                   \
+    if (damp && iso) return launch_decode<Real, D, true, true>(ws, A, s);
+    if (damp) return launch_decode<Real, D, true, false>(ws, A, s);
+    if (iso) return launch_decode<Real, D, false, true>(ws, A, s);
     return launch_decode<Real, D, false, false>(ws, A, s);
-    switch (ws->ens->D) {
-    case 8: { MBP_DISPATCH_D(8) }
-    case 16: { MBP_DISPATCH_D(16) }
-    case 32: { MBP_DISPATCH_D(32) }
-    case 64: { MBP_DISPATCH_D(64) }
+}
+
+template <class Real>
+static int dispatch_decode(mbp_workspace* ws, mbp::DecodeArgs<Real>& A, cudaStream_t s)
+{
+    const bool fast = sizeof(Real) == 4 && ws->cfg.damping == 0.0 &&
+                      ws->cfg.combining_mode == MBP_JOINT_GRAPH;
+    const int D = kernel_degree(ws->ens->Ds, fast);
+    if (fast) {
+        switch (D) {
+#define MBP_FAST(DD) case DD: return launch_decode<float, DD, false, false>(ws, reinterpret_cast<mbp::DecodeArgs<float>&>(A), s);
+        MBP_FAST(3) MBP_FAST(4) MBP_FAST(5) MBP_FAST(6) MBP_FAST(7) MBP_FAST(8) MBP_FAST(9) MBP_FAST(10)
+        MBP_FAST(11) MBP_FAST(12) MBP_FAST(13) MBP_FAST(14) MBP_FAST(15) MBP_FAST(16) MBP_FAST(20)
+        MBP_FAST(24) MBP_FAST(28) MBP_FAST(32) MBP_FAST(48) MBP_FAST(64)
+#undef MBP_FAST
+        default: return fail(MBP_EUNSUPPORTED, "check degree too large");
+        }
+    }
+    switch (D) {
+    case 8: return launch_variant<Real, 8>(ws, A, s);
+    case 16: return launch_variant<Real, 16>(ws, A, s);
+    case 32: return launch_variant<Real, 32>(ws, A, s);
+    case 64: return launch_variant<Real, 64>(ws, A, s);
     default: return fail(MBP_EUNSUPPORTED, "check degree too large");
     }
-#undef MBP_DISPATCH_D
 }
 
 template <class Real>
@@ -436,32 +467,35 @@ static int decode_chunk(mbp_workspace* ws, const uint8_t* noisy, const uint8_t* 
         fill_post_prior_kernel<Real><<<1024, 256, 0, s>>>(ws->noisy_w.as<unsigned>(), ws->Lmag.as<Real>(), G,
                                                           ens->n, P, ws->post.as<Real>());
         MBP_CUDA(cudaGetLastError());
-        MBP_CUDA(cudaMemsetAsync(ws->c2v.p, 0, (size_t)G * ens->C * ens->D * 32 * sizeof(Real), s));
+        MBP_CUDA(cudaMemsetAsync(ws->c2v.p, 0, (size_t)G * ens->C * ens->Ds * 32 * sizeof(Real), s));
     }
     MBP_CUDA(cudaMemsetAsync(ws->cnt.p, 0, 2 * (size_t)F * 4, s));
     MBP_CUDA(cudaMemsetAsync(ws->any_bad.p, 0, 8, s));
     MBP_CUDA(cudaMemsetAsync(ws->iters.p, 0xff, (size_t)F * 4, s));
     MBP_CUDA(cudaMemsetAsync(ws->barrier.p, 0, 8, s));
+    MBP_CUDA(cudaMemsetAsync(ws->work.p, 0, ws->work.bytes, s));
 
     mbp::DecodeArgs<Real> A;
     std::memset(&A, 0, sizeof A);
     A.n = ens->n; A.m = ens->m; A.u = ens->u; A.C = ens->C;
-    A.slots = (long long)ens->C * ens->D;
+    A.Ds = ens->Ds;
+    A.slots = (long long)ens->C * ens->Ds;
     A.deg = ens->deg.as<uint8_t>(); A.chk_ell = ens->chk_ell.as<int>();
     A.var_ptr = ens->var_ptr.as<int>(); A.var_edge = ens->var_slot.as<int>();
     A.dv = ens->dv_reg;
-    for (int l = 0; l <= ens->u; ++l) A.edge_off[l] = (long long)l * ens->m * ens->D;
+    for (int l = 0; l <= ens->u; ++l) A.edge_off[l] = (long long)l * ens->m * ens->Ds;
     A.G = G;
     A.c2v = ws->c2v.as<Real>(); A.post = ws->post.as<Real>(); A.v2c = ws->v2c.as<Real>();
     A.Lmag = ws->Lmag.as<Real>();
     A.noisy_w = ws->noisy_w.as<unsigned>(); A.syn_w = ws->syn_w.as<unsigned>();
     A.hard_w = ws->hard_w.as<unsigned>(); A.hist_w = record ? ws->hist_w.as<unsigned>() : nullptr;
     A.cnt = ws->cnt.as<int>(); A.any_bad = ws->any_bad.as<int>(); A.iters = ws->iters.as<int>();
-    A.barrier = ws->barrier.as<unsigned>(); A.sweeps_run = ws->sweeps.as<int>();
+    A.barrier = ws->barrier.as<unsigned>(); A.work = ws->work.as<unsigned>(); A.sweeps_run = ws->sweeps.as<int>();
     A.ts = ws->ts_cap ? ws->ts.as<unsigned long long>() : nullptr; A.ts_cap = ws->ts_cap;
     A.B = B; A.out_conv = conv; A.out_iters = iters; A.out_mism = mism;
     A.max_it = cfg.max_iterations; A.clamp = (Real)cfg.llr_clamp; A.damping = (Real)cfg.damping;
     A.sat = ens->sat;
+    if (A.Ds < 1 || A.slots < A.C) return fail(MBP_EINVAL, "internal: bad ELL stride");
     if ((rc = dispatch_decode<Real>(ws, A, s))) return rc;
     if ((rc = launch_words_to_rows(ws->hard_w.as<unsigned>(), ens->n, B, G, 1, ens->n, nb, corrected, nb, s)))
         return rc;
@@ -555,7 +589,7 @@ int mbp_syndrome_batch_device(mbp_workspace* ws, const uint8_t* keys, int64_t ba
             return rc;
         const long long items = (long long)G * ens->C;
         mbp::syndrome_words_kernel<<<(int)std::min<long long>((items + 255) / 256, 148LL * 32), 256, 0, s>>>(
-            ens->deg.as<uint8_t>(), ens->chk_ell.as<int>(), ens->D, ens->n, ens->C, G, ws->noisy_w.as<unsigned>(),
+            ens->deg.as<uint8_t>(), ens->chk_ell.as<int>(), ens->Ds, ens->n, ens->C, G, ws->noisy_w.as<unsigned>(),
             ws->syn_w.as<unsigned>());
         MBP_CUDA(cudaGetLastError());
         if ((rc = launch_words_to_rows(ws->syn_w.as<unsigned>(), ens->C, B, G, ens->u, ens->m, mb,
@@ -625,7 +659,7 @@ int mbp_workspace_read_c2v(mbp_workspace* ws, int64_t frame, double* c2v)
     const mbp_ensemble* ens = ws->ens;
     DeviceGuard dg(ens->device);
     MBP_CUDA(cudaDeviceSynchronize());
-    const char* base = ws->c2v.as<char>() + ((size_t)(frame / 32) * ens->C * ens->D * 32) * ws->real_size;
+    const char* base = ws->c2v.as<char>() + ((size_t)(frame / 32) * ens->C * ens->Ds * 32) * ws->real_size;
     return read_lane(ws, base, ens->E, frame, c2v, ens->ref2slot.as<int>());
 }
 
@@ -637,7 +671,7 @@ int mbp_workspace_read_v2c(mbp_workspace* ws, int64_t frame, double* v2c)
     const mbp_ensemble* ens = ws->ens;
     DeviceGuard dg(ens->device);
     MBP_CUDA(cudaDeviceSynchronize());
-    const char* base = ws->v2c.as<char>() + ((size_t)(frame / 32) * ens->C * ens->D * 32) * ws->real_size;
+    const char* base = ws->v2c.as<char>() + ((size_t)(frame / 32) * ens->C * ens->Ds * 32) * ws->real_size;
     return read_lane(ws, base, ens->E, frame, v2c, ens->ref2slot.as<int>());
 }
 
