@@ -8,6 +8,7 @@ library is missing or no GPU is present the call raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from .build import LIB
@@ -86,7 +87,7 @@ def load(path: Path | None = None) -> C.CDLL:
     """Load (never build) the library; raises if it is missing."""
     global _LIB
     if _LIB is None:
-        p = Path(path or LIB)
+        p = Path(path or os.environ.get("MBP_LIB") or LIB)
         if not p.exists():
             raise MBPError(f"{p} not built: run `python -m paper_2001_07979_b200.build` "
                            "(the decoder has no CPU fallback)")

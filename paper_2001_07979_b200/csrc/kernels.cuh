@@ -43,19 +43,35 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p)
     return v;
 }
 
-// predicated loads/stores without branches (uniform or per-lane predicate)
+// predicated loads/stores without branches (uniform or per-lane predicate).
+// ld_cg_pred leaves the destination undefined when the predicate is off
+// (callers mask those values); ld_cg_if zero-fills.
+__device__ __forceinline__ float ld_cg_pred(const float* p, bool pred)
+{
+    float v;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.cg.f32 %0, [%1];\n\t}"
+                 : "=f"(v) : "l"(p), "r"((int)pred));
+    return v;
+}
+__device__ __forceinline__ double ld_cg_pred(const double* p, bool pred)
+{
+    double v;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.cg.f64 %0, [%1];\n\t}"
+                 : "=d"(v) : "l"(p), "r"((int)pred));
+    return v;
+}
 __device__ __forceinline__ float ld_cg_if(const float* p, bool pred)
 {
     float v = 0.0f;
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.cg.f32 %0, [%1];\n\t}"
-                 : "+f"(v) : "l"(p), "r"((int)pred) : "memory");
+                 : "+f"(v) : "l"(p), "r"((int)pred));
     return v;
 }
 __device__ __forceinline__ double ld_cg_if(const double* p, bool pred)
 {
     double v = 0.0;
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.cg.f64 %0, [%1];\n\t}"
-                 : "+d"(v) : "l"(p), "r"((int)pred) : "memory");
+                 : "+d"(v) : "l"(p), "r"((int)pred));
     return v;
 }
 __device__ __forceinline__ void st_if(float* p, float v, bool pred)
@@ -90,15 +106,21 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar)
 }
 
 // ---------------------------------------------------------------------------
-// Eq. 6 in the phi domain (fp32).  phi(x) = -ln tanh(x/2) = log1p(2/expm1(x))
-// is an involution on [0, inf]; for the other-edge set N(j)\a,
-//   |2 atanh(prod tanh(x_b/2))| = phi( sum phi(|x_b|) ),
-//   sign = prod sign(x_b).
-// Exclusive sums come from prefix + suffix sums (no total-minus-own
-// cancellation; phi(0) = inf propagates to an exact 0 output).  |x| >= sat
-// contributes phi = 0: that is where the reference's float64 tanh(x/2)
-// rounds to exactly 1.0, and all-others-saturated then gives +-clamp as in
-// the `prod >= 1.0` branch of c2v_pass (_kernels.py:249-252).
+// Eq. 6 in fp32, complement-product form.  The reference rule
+//   c2v_a = (-1)^z_j * 2 atanh( prod_{b != a} tanh(x_b / 2) )      (clamped)
+// is evaluated with |tanh(x/2)| = 1 - c, c = 2u/(1+u), u = e^-|x|, and the
+// magnitude of the product carried as its complement Q = 1 - prod t_b,
+// combined by the exact identity 1 - (1-Q)(1-c) = Q + c(1 - Q).  Q keeps
+// full relative precision where the plain fp32 product of tanh values
+// rounds to 1 (|x| >~ 17, the failure of naive fp32 tanh);
+// the output is 2 atanh(1 - Q) = ln((2 - Q) / Q).  Exclusive products come
+// from prefix and suffix complements (no division), padding slots have c = 0
+// (t = 1, neutral), and |x| >= sat also gives c = 0: that is where the
+// reference's float64 tanh(x/2) rounds to exactly 1.0, and all-others-
+// saturated then yields Q = 0 -> +-clamp as in its `prod >= 1.0` branch
+// (_kernels.py:249-252).  4 MUFU + ~15 FMA-pipe ops per edge; max error
+// |d| <= 4e-7 * max(|ref|, 1) against the exact rule (tools/ notes,
+// DESIGN.md §3).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ float ex2_approx(float x)
 {
@@ -114,56 +136,46 @@ __device__ __forceinline__ float lg2_approx(float x)
     return y;
 }
 
-// phi(x) = ln((1+t)/(1-t)), t = e^-x, branch-free, 3 MUFU + ~16 FMA, max
-// relative error ~7e-7 over [0, inf] (phi(0) = inf, phi(inf) = 0):
-//   1 - t from its Taylor series below x = 1/4 (no cancellation),
-//   2 atanh(t) series once t < 1/8 (no lg2 of a ratio near 1).
-__device__ __forceinline__ float phi_f32(float x)
+__device__ __forceinline__ float rcp_approx(float x)
 {
-    const float t = ex2_approx(-1.44269504088896341f * x);
-    const float dser = x * (1.0f - x * (0.5f - x * (1.0f / 6 - x * (1.0f / 24 - x * (1.0f / 120 - x * (1.0f / 720))))));
-    const float den = x < 0.25f ? dser : 1.0f - t;
-    const float num = 2.0f - den;
-    const float L = (lg2_approx(num) - lg2_approx(den)) * 0.69314718055994531f;
-    const float t2 = t * t;
-    const float ser = 2.0f * t * (1.0f + t2 * (1.0f / 3 + t2 * (1.0f / 5 + t2 * (1.0f / 7 + t2 * (1.0f / 9)))));
-    return t < 0.125f ? ser : L;
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
 }
-
-template <bool Wide> struct SignMaskT { using T = unsigned; };
-template <> struct SignMaskT<true> { using T = unsigned long long; };
-template <int D> struct SignMask { using T = typename SignMaskT<(D > 32)>::T; };
 
 template <int D>
 __device__ __forceinline__ void c2v_rule(const float (&x)[D], int d, unsigned flip, float clamp,
                                          float sat, float (&out)[D])
 {
-    using M = typename SignMask<D>::T;
-    float ph[D];
-    M sg = 0;
+    // x[k] for k >= d may be garbage (predicated-off loads): masked here
+    float c[D];
+    unsigned sb[D];
+    unsigned tot = flip << 31;  // syndrome sign (-1)^z_j folded into the parity
 #pragma unroll
     for (int k = 0; k < D; ++k) {
+        const bool in = k < d;
         const float a = fabsf(x[k]);
-        const float f = phi_f32(a);
-        ph[k] = (k < d && a < sat) ? f : 0.0f;   // padding slots contribute nothing
-        sg |= (M)(x[k] < 0.0f) << k;             // padding x == 0: sign bit 0
+        const float u = ex2_approx(-1.44269504088896341f * a);
+        const float ck = 2.0f * u * rcp_approx(1.0f + u);
+        c[k] = (in && a < sat) ? ck : 0.0f;
+        sb[k] = in ? (__float_as_uint(x[k]) & 0x80000000u) : 0u;
+        tot ^= sb[k];
     }
-    float suf[D];
-    float s = 0.0f;
+    float qs[D];
+    float q = 0.0f;
 #pragma unroll
     for (int k = D - 1; k >= 0; --k) {
-        suf[k] = s;
-        s += ph[k];
+        qs[k] = q;
+        q = fmaf(c[k], 1.0f - q, q);
     }
-    const unsigned par = (sizeof(M) == 8 ? __popcll((unsigned long long)sg) : __popc((unsigned)sg)) & 1u;
-    float pre = 0.0f;
+    float qp = 0.0f;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-        const float ex = pre + suf[k];
-        pre += ph[k];
-        const float mag = fminf(phi_f32(ex), clamp);
-        const unsigned neg = par ^ (unsigned)((sg >> k) & 1) ^ flip;
-        out[k] = neg ? -mag : mag;
+        const float r = 1.0f - qp;
+        const float qx = fmaf(qs[k], r, qp);
+        qp = fmaf(c[k], r, qp);
+        const float mag = fminf((lg2_approx(2.0f - qx) - lg2_approx(qx)) * 0.69314718055994531f, clamp);
+        out[k] = __uint_as_float(__float_as_uint(mag) | (tot ^ sb[k]));
     }
 }
 
@@ -197,6 +209,10 @@ __device__ __forceinline__ void c2v_rule(const double (&x)[D], int d, unsigned f
 template <class Real> __device__ __forceinline__ Real clampr(Real v, Real c)
 {
     return v > c ? c : (v < -c ? -c : v);
+}
+template <> __device__ __forceinline__ float clampr<float>(float v, float c)
+{
+    return fminf(fmaxf(v, -c), c);
 }
 
 // ---------------------------------------------------------------------------
@@ -480,8 +496,11 @@ __device__ __forceinline__ unsigned group_mask(const int* cprev, int g, int lane
     return __ballot_sync(kFull, ld_cg(cprev + g * 32 + lane) != 0);
 }
 
+#ifndef MBP_FP32_MIN_BLOCKS
+#define MBP_FP32_MIN_BLOCKS 4
+#endif
 template <class Real, int D>
-constexpr int decode_min_blocks() { return (sizeof(Real) == 4 && D <= 16) ? 4 : 2; }
+constexpr int decode_min_blocks() { return (sizeof(Real) == 4 && D <= 16) ? MBP_FP32_MIN_BLOCKS : 2; }
 
 constexpr int kDecodeThreads = 256;
 
