@@ -269,22 +269,18 @@ struct DecodeArgs {
 };
 
 // Check phase item: check j of group g at sweep t; `act` = lanes (frames)
-// still decoding.  Reads post_{t-1}, c2v_{t-1}, writes c2v_t.  Branch-free
-// over the D slots (D = the launch's degree bound): slots k >= d(j) are
-// predicated off, so the only divergence is none.
+// still decoding.  Reads post_{t-1}, c2v_{t-1}, writes c2v_t.  The row's
+// variable ids, degree and syndrome word come from the warp's shared-memory
+// stage of its work chunk (one coalesced load per chunk, not per item), so
+// an item costs one memory round trip.  Branch-free over the D slots
+// (D = the launch's degree bound): slots k >= d are predicated off.
 template <class Real, int D, bool DAMP, bool ISO>
 __device__ __forceinline__ void check_item(const DecodeArgs<Real>& A, int g, int j, int t,
-                                           unsigned act, int lane)
+                                           unsigned act, int lane, const int* srow, int d,
+                                           unsigned synword, Real L)
 {
-    const int d = ld_ro(A.deg + j);
-    constexpr int NC = (D + 31) / 32;
-    const int* row = A.chk_ell + j * A.Ds;
-    int vid[NC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) vid[c] = (c * 32 + lane < d) ? ld_ro(row + c * 32 + lane) : 0;
     const bool live = (act >> lane) & 1u;
-    const unsigned flip = (ld_ro(A.syn_w + (size_t)g * A.C + j) >> lane) & 1u;
-    const Real L = ld_ro(A.Lmag + g * 32 + lane);
+    const unsigned flip = (synword >> lane) & 1u;
     const int mat = ISO ? j / A.m : 0;
     Real* c2v_row = A.c2v + ((size_t)g * A.slots + (size_t)j * A.Ds) * 32 + lane;
     Real* v2c_row = DAMP ? A.v2c + ((size_t)g * A.slots + (size_t)j * A.Ds) * 32 + lane : nullptr;
@@ -296,8 +292,7 @@ __device__ __forceinline__ void check_item(const DecodeArgs<Real>& A, int g, int
         const unsigned* nw = A.noisy_w + (size_t)g * A.n;
 #pragma unroll
         for (int k = 0; k < D; ++k) {
-            const int v = __shfl_sync(kFull, vid[k >> 5], k & 31);
-            const unsigned w = k < d ? ld_ro(nw + v) : 0u;
+            const unsigned w = k < d ? ld_ro(nw + srow[k]) : 0u;
             x[k] = k < d ? (((w >> lane) & 1u) ? -L : L) : Real(0);
         }
         if (DAMP) {
@@ -308,9 +303,8 @@ __device__ __forceinline__ void check_item(const DecodeArgs<Real>& A, int g, int
         Real p[D], q[D];
 #pragma unroll
         for (int k = 0; k < D; ++k) {
-            const int v = __shfl_sync(kFull, vid[k >> 5], k & 31);
             const bool pk = live && k < d;
-            p[k] = ld_cg_if(postg + (unsigned)v * 32u, pk);
+            p[k] = ld_cg_if(postg + (unsigned)srow[k] * 32u, pk);
             q[k] = ld_cg_if(c2v_row + k * 32, pk);
         }
         if (DAMP) {
@@ -334,44 +328,35 @@ __device__ __forceinline__ void check_item(const DecodeArgs<Real>& A, int g, int
 // Variable phase, regular column degree DV, NV variables per warp pass
 // (independent load streams in flight): joint posterior prior + sum of every
 // matrix's c2v in ascending edge order (posterior_pass, _kernels.py:293-301),
-// hard decision post < 0 (ties -> 0) as a ballot (hard_pass).
+// hard decision post < 0 (ties -> 0) as a ballot (hard_pass).  Edge slots,
+// noisy words and previous hard words come from the chunk's shared stage.
 template <class Real, int DV, int NV>
 __device__ __forceinline__ void var_items_regular(const DecodeArgs<Real>& A, int g, int i0, int nv, int t,
-                                                  unsigned act, int lane)
+                                                  unsigned act, int lane, const int* sedge, int sstride,
+                                                  const unsigned* snoisy, const unsigned* sold, Real L)
 {
     const bool live = (act >> lane) & 1u;
     const Real* c2vg = A.c2v + (size_t)g * A.slots * 32 + lane;
-    const Real L = ld_ro(A.Lmag + g * 32 + lane);
-    int eid[NV];
-    unsigned nwd[NV], old[NV];
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-        const int i = i0 + v;
-        const bool ok = v < nv;
-        eid[v] = (ok && lane < DV) ? ld_ro(A.var_edge + i * DV + lane) : 0;
-        nwd[v] = ok ? ld_ro(A.noisy_w + (size_t)g * A.n + i) : 0u;
-        old[v] = (ok && lane == 0) ? ld_cg(A.hard_w + (size_t)g * A.n + i) : 0u;
-    }
     Real c[NV][DV];
 #pragma unroll
     for (int v = 0; v < NV; ++v)
 #pragma unroll
         for (int k = 0; k < DV; ++k) {
-            const int e = __shfl_sync(kFull, eid[v], k);
+            const int e = v < nv ? sedge[v * sstride + k] : 0;
             c[v][k] = ld_cg_if(c2vg + (unsigned)e * 32u, live && v < nv);
         }
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
         if (v >= nv) break;
         const int i = i0 + v;
-        Real acc = ((nwd[v] >> lane) & 1u) ? -L : L;
+        Real acc = ((snoisy[v] >> lane) & 1u) ? -L : L;
 #pragma unroll
         for (int k = 0; k < DV; ++k) acc += c[v][k];
         const size_t w = (size_t)g * A.n + i;
         st_if(A.post + w * 32 + lane, acc, live);
         const unsigned neg = __ballot_sync(kFull, acc < Real(0));
         if (lane == 0) {
-            const unsigned hw = (neg & act) | (old[v] & ~act);
+            const unsigned hw = (neg & act) | (sold[v] & ~act);
             A.hard_w[w] = hw;
             if (A.hist_w) A.hist_w[((size_t)t * A.G) * A.n + w] = hw;
         }
@@ -479,21 +464,104 @@ __device__ __forceinline__ void stamp(const DecodeArgs<Real>& A, int& k)
     ++k;
 }
 
-// Dynamic work distribution: warps claim chunks of kChunk consecutive items
-// from a per-phase counter (balanced tails; consecutive items stay in one
-// group so the group's active mask is loaded once per chunk).
-constexpr int kChunk = 16;
+// Dynamic work distribution: warps claim chunks of consecutive items from a
+// per-phase counter (balanced tails); a chunk's graph rows and per-item words
+// are staged in the warp's shared-memory slice with one coalesced load.
+template <int D> struct Chunk {
+    static constexpr int CH = D <= 16 ? 32 : 8;   // items per claim (check / variable phases)
+    static constexpr int SD = D | 1;               // odd smem row stride: conflict-free staging
+};
+constexpr int kSynChunk = 16;                      // syndrome-phase items (32 checks each)
 
-__device__ __forceinline__ int claim(unsigned* counter, int lane)
+// items per claim: CH for large phases, fewer when a phase has less than
+// ~4 chunks per warp (small batches), so all warps get work
+__device__ __forceinline__ int chunk_size(int total, int nwarps, int CH)
+{
+    return max(1, min(CH, total / (4 * nwarps)));
+}
+
+__device__ __forceinline__ int claim(unsigned* counter, int lane, int n)
 {
     unsigned base = 0;
-    if (lane == 0) base = atomicAdd(counter, (unsigned)kChunk);
+    if (lane == 0) base = atomicAdd(counter, (unsigned)n);
     return (int)__shfl_sync(kFull, base, 0);
 }
 
 __device__ __forceinline__ unsigned group_mask(const int* cprev, int g, int lane)
 {
     return __ballot_sync(kFull, ld_cg(cprev + g * 32 + lane) != 0);
+}
+
+// one claimed chunk of the check phase: items [base, end) of the G*C space
+template <class Real, int D, bool DAMP, bool ISO>
+__device__ __forceinline__ void check_chunk(const DecodeArgs<Real>& A, int base, int end, int t,
+                                            const int* cprev, int lane, int* s_idx, unsigned* s_w,
+                                            int* s_d)
+{
+    constexpr int SD = Chunk<D>::SD;
+    const int rows = end - base;
+    if (lane < rows) {
+        const int item = base + lane;
+        const int j = item % A.C;
+        const int d = ld_ro(A.deg + j);
+        s_d[lane] = d;
+        s_w[lane] = ld_ro(A.syn_w + item);  // syn_w index == item (g*C + j)
+        const int* row = A.chk_ell + j * A.Ds;
+#pragma unroll
+        for (int k = 0; k < D; ++k)
+            if (k < d) s_idx[lane * SD + k] = ld_ro(row + k);
+    }
+    __syncwarp();
+    int g = base / A.C;
+    int j = base - g * A.C;
+    unsigned act = group_mask(cprev, g, lane);
+    Real L = ld_ro(A.Lmag + g * 32 + lane);
+    for (int r = 0; r < rows; ++r) {
+        if (act) check_item<Real, D, DAMP, ISO>(A, g, j, t, act, lane, s_idx + r * SD, s_d[r], s_w[r], L);
+        if (++j == A.C && r + 1 < rows) {
+            j = 0;
+            ++g;
+            act = group_mask(cprev, g, lane);
+            L = ld_ro(A.Lmag + g * 32 + lane);
+        }
+    }
+    __syncwarp();
+}
+
+// one claimed chunk of the variable phase (regular column degree DV)
+template <class Real, int DV>
+__device__ __forceinline__ void var_chunk_regular(const DecodeArgs<Real>& A, int base, int end, int t,
+                                                  const int* cprev, int lane, int* s_idx, unsigned* s_w,
+                                                  unsigned* s_old)
+{
+    constexpr int SV = DV | 1;
+    const int rows = end - base;
+    if (lane < rows) {
+        const int item = base + lane;            // == g*n + i
+        const int i = item % A.n;
+        s_w[lane] = ld_ro(A.noisy_w + item);
+        s_old[lane] = ld_cg(A.hard_w + item);
+        const int* row = A.var_edge + i * DV;
+#pragma unroll
+        for (int k = 0; k < DV; ++k) s_idx[lane * SV + k] = ld_ro(row + k);
+    }
+    __syncwarp();
+    int r = 0;
+    while (r < rows) {
+        const int item = base + r;
+        const int g = item / A.n;
+        const int i = item - g * A.n;
+        const int span = min(rows - r, A.n - i);
+        const unsigned act = group_mask(cprev, g, lane);
+        const Real L = ld_ro(A.Lmag + g * 32 + lane);
+        if (act) {
+            for (int k = 0; k < span; k += 2)
+                var_items_regular<Real, DV, 2>(A, g, i + k, min(2, span - k), t, act, lane,
+                                               s_idx + (r + k) * SV, SV, s_w + r + k, s_old + r + k, L);
+        }
+        r += span;
+    }
+    __syncwarp();
 }
 
 #ifndef MBP_FP32_MIN_BLOCKS
@@ -509,10 +577,20 @@ __global__ void __launch_bounds__(kDecodeThreads, decode_min_blocks<Real, D>())
 decode_kernel(const DecodeArgs<Real> A)
 {
     const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const int nthreads = gridDim.x * blockDim.x;
+    const int nwarps = nthreads >> 5;
     const int F = A.G * 32;
     const int cblk = (A.C + 31) / 32;
+    constexpr int CH = Chunk<D>::CH;
+    constexpr int SLICE = CH * (Chunk<D>::SD > 9 ? Chunk<D>::SD : 9);   // ints per warp (check or var rows)
+    __shared__ int s_idx_all[kDecodeThreads / 32][SLICE];
+    __shared__ unsigned s_w_all[kDecodeThreads / 32][CH];
+    __shared__ unsigned s_x_all[kDecodeThreads / 32][CH];
+    int* s_idx = s_idx_all[warp];
+    unsigned* s_w = s_w_all[warp];
+    unsigned* s_x = s_x_all[warp];
     int ts_k = 0;
     int wc = 0;  // next work counter
     stamp(A, ts_k);
@@ -520,8 +598,9 @@ decode_kernel(const DecodeArgs<Real> A)
     // iteration 0: the uncorrected key against all u*m syndromes (_kernels.py:358-365)
     {
         const int total = A.G * cblk;
-        for (int base = claim(A.work + wc, lane); base < total; base = claim(A.work + wc, lane))
-            for (int item = base; item < min(base + kChunk, total); ++item)
+        for (int base = claim(A.work + wc, lane, kSynChunk); base < total;
+             base = claim(A.work + wc, lane, kSynChunk))
+            for (int item = base; item < min(base + kSynChunk, total); ++item)
                 syncheck_item<Real>(A, item / cblk, item % cblk, 0, kFull, lane);
         ++wc;
     }
@@ -545,42 +624,34 @@ decode_kernel(const DecodeArgs<Real> A)
 
         {   // check phase
             const int total = A.G * A.C;
-            for (int base = claim(A.work + wc, lane); base < total; base = claim(A.work + wc, lane)) {
-                const int end = min(base + kChunk, total);
-                int g = base / A.C;
-                unsigned act = group_mask(cprev, g, lane);
-                for (int item = base; item < end; ++item) {
-                    const int gi = item / A.C;
-                    if (gi != g) { g = gi; act = group_mask(cprev, g, lane); }
-                    if (act) check_item<Real, D, DAMP, ISO>(A, g, item - g * A.C, t, act, lane);
-                }
-            }
+            const int ch = chunk_size(total, nwarps, CH);
+            for (int base = claim(A.work + wc, lane, ch); base < total; base = claim(A.work + wc, lane, ch))
+                check_chunk<Real, D, DAMP, ISO>(A, base, min(base + ch, total), t, cprev, lane,
+                                                s_idx, s_w, reinterpret_cast<int*>(s_x));
             ++wc;
         }
         grid_barrier(A.barrier);
         stamp(A, ts_k);
         {   // variable phase
             const int total = A.G * A.n;
-            for (int base = claim(A.work + wc, lane); base < total; base = claim(A.work + wc, lane)) {
-                const int end = min(base + kChunk, total);
-                int item = base;
-                while (item < end) {
-                    const int g = item / A.n;
-                    const int i = item - g * A.n;
-                    const unsigned act = group_mask(cprev, g, lane);
-                    const int span = min(end - item, A.n - i);  // items left in this group
-                    if (act) {
-                        if (!ISO && A.dv == 6) {
-                            for (int k = 0; k < span; k += 2)
-                                var_items_regular<Real, 6, 2>(A, g, i + k, min(2, span - k), t, act, lane);
-                        } else if (!ISO && A.dv == 9) {
-                            for (int k = 0; k < span; k += 2)
-                                var_items_regular<Real, 9, 2>(A, g, i + k, min(2, span - k), t, act, lane);
-                        } else {
+            const int ch = chunk_size(total, nwarps, CH);
+            for (int base = claim(A.work + wc, lane, ch); base < total; base = claim(A.work + wc, lane, ch)) {
+                const int end = min(base + ch, total);
+                if (!ISO && A.dv == 6) {
+                    var_chunk_regular<Real, 6>(A, base, end, t, cprev, lane, s_idx, s_w, s_x);
+                } else if (!ISO && A.dv == 9) {
+                    var_chunk_regular<Real, 9>(A, base, end, t, cprev, lane, s_idx, s_w, s_x);
+                } else {
+                    int item = base;
+                    while (item < end) {
+                        const int g = item / A.n;
+                        const int i = item - g * A.n;
+                        const unsigned act = group_mask(cprev, g, lane);
+                        const int span = min(end - item, A.n - i);
+                        if (act)
                             for (int k = 0; k < span; ++k) var_item<Real, ISO>(A, g, i + k, t, act, lane);
-                        }
+                        item += span;
                     }
-                    item += span;
                 }
             }
             ++wc;
@@ -589,8 +660,9 @@ decode_kernel(const DecodeArgs<Real> A)
         stamp(A, ts_k);
         {   // syndrome phase
             const int total = A.G * cblk;
-            for (int base = claim(A.work + wc, lane); base < total; base = claim(A.work + wc, lane)) {
-                const int end = min(base + kChunk, total);
+            for (int base = claim(A.work + wc, lane, kSynChunk); base < total;
+                 base = claim(A.work + wc, lane, kSynChunk)) {
+                const int end = min(base + kSynChunk, total);
                 int g = base / cblk;
                 unsigned act = group_mask(cprev, g, lane);
                 for (int item = base; item < end; ++item) {
