@@ -64,7 +64,8 @@ typedef enum {
 enum {
     MBP_RECORD_HISTORY = 1,  /* keep the hard decision after every sweep     */
     MBP_KEEP_STATE = 2,      /* keep posteriors/messages readable after decode */
-    MBP_PROFILE_PHASES = 4   /* record a globaltimer stamp at every phase barrier */
+    MBP_PROFILE_PHASES = 4,  /* record a globaltimer stamp at every phase barrier */
+    MBP_NO_COMPACTION = 8    /* never repack undecided frames into dense groups   */
 };
 
 typedef struct mbp_decoder_config {
@@ -150,7 +151,9 @@ int mbp_workspace_read_history(mbp_workspace *ws, int64_t frame, int32_t rows, u
 
 /* globaltimer (ns) stamps of the last decode's chunk (MBP_PROFILE_PHASES):
  * kernel start, then after each grid barrier (3 per executed sweep: check,
- * variable, syndrome phases, plus the final stop test), then kernel end.  */
+ * variable, syndrome phases, plus the final stop test), then kernel end;
+ * *count of those are written, followed (cap permitting) by 4 compaction
+ * stamps: start, slot maps built, arrays moved, done (0 if none).        */
 int mbp_workspace_read_phase_times(mbp_workspace *ws, uint64_t *ns, int32_t cap, int32_t *count);
 
 /* ---- single phases on explicit per-edge messages of ONE frame ------------
@@ -177,6 +180,9 @@ void mbp_host_free(void *p);
  * pointer may be NULL.                                                      */
 int mbp_workspace_last_timing(mbp_workspace *ws, float *decode_kernel_ms, float *e2e_ms,
                               int32_t *sweeps_run);
+/* sweeps the last chunk executed and the sweep at whose start undecided
+ * frames were compacted into dense groups (0: no compaction).             */
+int mbp_workspace_last_stats(mbp_workspace *ws, int32_t *sweeps_run, int32_t *compaction_sweep);
 
 #ifdef __cplusplus
 }

@@ -16,7 +16,7 @@ from .build import LIB
 MBP_OK, MBP_EINVAL, MBP_ECUDA, MBP_EUNSUPPORTED, MBP_ENOMEM = range(5)
 MBP_JOINT_GRAPH, MBP_ISOLATED_PER_MATRIX = 0, 1
 MBP_FP32_PHI, MBP_FP64_TANH = 0, 1
-MBP_RECORD_HISTORY, MBP_KEEP_STATE, MBP_PROFILE_PHASES = 1, 2, 4
+MBP_RECORD_HISTORY, MBP_KEEP_STATE, MBP_PROFILE_PHASES, MBP_NO_COMPACTION = 1, 2, 4, 8
 
 #: every symbol include/mbp.h declares (checked by tests/test_native_abi.py)
 EXPORTS = (
@@ -28,7 +28,7 @@ EXPORTS = (
     "mbp_workspace_read_posterior", "mbp_workspace_read_c2v", "mbp_workspace_read_v2c",
     "mbp_workspace_read_history", "mbp_workspace_read_phase_times",
     "mbp_c2v_pass", "mbp_v2c_pass", "mbp_posterior_pass",
-    "mbp_host_alloc", "mbp_host_free", "mbp_workspace_last_timing",
+    "mbp_host_alloc", "mbp_host_free", "mbp_workspace_last_timing", "mbp_workspace_last_stats",
 )
 
 
@@ -78,6 +78,7 @@ _SIGS = {
     "mbp_host_alloc": ([C.c_size_t], _VP),
     "mbp_host_free": ([_VP], None),
     "mbp_workspace_last_timing": ([_VP, C.POINTER(C.c_float), C.POINTER(C.c_float), C.POINTER(C.c_int32)], C.c_int),
+    "mbp_workspace_last_stats": ([_VP, C.POINTER(C.c_int32), C.POINTER(C.c_int32)], C.c_int),
 }
 
 _LIB = None

@@ -21,7 +21,7 @@ CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libmbp_b200.so"
 SOURCES = [CSRC / "mbp.cu"]
-DEPS = SOURCES + [CSRC / "kernels.cuh", ROOT / "include" / "mbp.h"]
+DEPS = SOURCES + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "mbp.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -9,14 +9,9 @@
 // rows of different degree never diverge a warp.  Bits (noisy key, hard
 // decision, syndrome) are 32-frame words: word[g*n + i] bit f = frame 32g+f.
 //
-// One persistent cooperative kernel runs the whole flooding decode
-// (decode_loop, _kernels.py:323-379): per sweep a check phase (Eq. 6,
-// c2v_pass _kernels.py:230-261, with the variable-to-check message formed on
-// the fly in APP form v2c = clamp(post - c2v), exact because the reference's
-// joint `total` IS the posterior sum, _kernels.py:276-279 vs 296-300), a
-// variable phase (posterior Eq. 2 + hard decision, _kernels.py:293-307), and
-// a syndrome phase (mismatch_count, _kernels.py:310-320) whose per-frame
-// counts drive early termination; phases are separated by a grid barrier.
+// This header holds the device primitives (cache-control loads, the grid
+// barrier, the check-node rule, bit transposes, the Alice-side syndrome and
+// the single-phase kernels); the persistent decode kernel is in decode.cuh.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -215,479 +210,7 @@ template <> __device__ __forceinline__ float clampr<float>(float v, float c)
     return fminf(fmaxf(v, -c), c);
 }
 
-// ---------------------------------------------------------------------------
-// decode kernel arguments
-//
-// Internal edge numbering (padded ELL): edge k of stacked check j is slot
-// j*D + k, D = the kernel's degree bound.  A check's var ids chk_ell[j*D..]
-// and its message lines are contiguous and need no chk_ptr lookup (one
-// dependent load less per item); slot order is monotone in the reference's
-// edge order, so ascending var_edge lists and matrix boundaries
-// (edge_off[l] = l*m*D) keep the reference's summation order.
-// ---------------------------------------------------------------------------
-template <class Real>
-struct DecodeArgs {
-    // graph
-    int n, m, u, C;
-    int Ds;                            // ELL row stride (= max check degree)
-    long long slots;                   // C * Ds
-    const uint8_t* __restrict__ deg;   // [C] row degree
-    const int* __restrict__ chk_ell;   // [C*Ds] var ids (pad 0)
-    const int* __restrict__ var_ptr;   // [n+1] into var_edge (CSR; unused when dv > 0)
-    const int* __restrict__ var_edge;  // [E] slot ids, ascending per variable
-    int dv;                            // regular column degree, 0 if irregular
-    long long edge_off[kMaxU + 1];     // slot offsets of the matrices
-    // batch
-    int G;                       // groups of 32 frames
-    // state
-    Real* __restrict__ c2v;      // [G][slots][32]
-    Real* __restrict__ post;     // [G][P][n][32], P = ISO ? u+1 : 1
-    Real* __restrict__ v2c;      // [G][slots][32] (damping only)
-    const Real* __restrict__ Lmag;         // [G*32] prior magnitude per frame
-    const unsigned* __restrict__ noisy_w;  // [G][n]
-    const unsigned* __restrict__ syn_w;    // [G][C]
-    unsigned* __restrict__ hard_w;         // [G][n]
-    unsigned* __restrict__ hist_w;         // [(T+1)][G][n] or null
-    int* __restrict__ cnt;       // [2][G*32] mismatch counts by sweep parity
-    int* __restrict__ any_bad;   // [2]
-    int* __restrict__ iters;     // [G*32] first converged sweep, -1 unset
-    unsigned* __restrict__ barrier;  // [2]
-    unsigned* __restrict__ work;     // [3*(T+1)+1] dynamic work counters, zeroed per launch
-    int* __restrict__ sweeps_run;    // [1]
-    unsigned long long* __restrict__ ts;  // phase timestamps (globaltimer ns) or null
-    int ts_cap;
-    // outputs (per frame, batch B)
-    int B;
-    uint8_t* __restrict__ out_conv;
-    int* __restrict__ out_iters;
-    int* __restrict__ out_mism;
-    // config
-    int max_it;
-    Real clamp;
-    Real damping;
-    float sat;
-};
-
-// Check phase item: check j of group g at sweep t; `act` = lanes (frames)
-// still decoding.  Reads post_{t-1}, c2v_{t-1}, writes c2v_t.  The row's
-// variable ids, degree and syndrome word come from the warp's shared-memory
-// stage of its work chunk (one coalesced load per chunk, not per item), so
-// an item costs one memory round trip.  Branch-free over the D slots
-// (D = the launch's degree bound): slots k >= d are predicated off.
-template <class Real, int D, bool DAMP, bool ISO>
-__device__ __forceinline__ void check_item(const DecodeArgs<Real>& A, int g, int j, int t,
-                                           unsigned act, int lane, const int* srow, int d,
-                                           unsigned synword, Real L)
-{
-    const bool live = (act >> lane) & 1u;
-    const unsigned flip = (synword >> lane) & 1u;
-    const int mat = ISO ? j / A.m : 0;
-    Real* c2v_row = A.c2v + ((size_t)g * A.slots + (size_t)j * A.Ds) * 32 + lane;
-    Real* v2c_row = DAMP ? A.v2c + ((size_t)g * A.slots + (size_t)j * A.Ds) * 32 + lane : nullptr;
-    const Real* postg = A.post + ((size_t)g * (ISO ? A.u + 1 : 1) + mat) * A.n * 32 + lane;
-
-    Real x[D];
-    if (t == 1) {
-        // sweep 1 reads the UNCLAMPED prior (decode_loop init, _kernels.py:353-355)
-        const unsigned* nw = A.noisy_w + (size_t)g * A.n;
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-            const unsigned w = k < d ? ld_ro(nw + srow[k]) : 0u;
-            x[k] = k < d ? (((w >> lane) & 1u) ? -L : L) : Real(0);
-        }
-        if (DAMP) {
-#pragma unroll
-            for (int k = 0; k < D; ++k) st_if(v2c_row + k * 32, x[k], live && k < d);
-        }
-    } else {
-        Real p[D], q[D];
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-            const bool pk = live && k < d;
-            p[k] = ld_cg_if(postg + (unsigned)srow[k] * 32u, pk);
-            q[k] = ld_cg_if(c2v_row + k * 32, pk);
-        }
-        if (DAMP) {
-#pragma unroll
-            for (int k = 0; k < D; ++k) {
-                const Real old = ld_cg_if(v2c_row + k * 32, live && k < d);
-                x[k] = clampr((Real(1) - A.damping) * (p[k] - q[k]) + A.damping * old, A.clamp);
-                st_if(v2c_row + k * 32, x[k], live && k < d);
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < D; ++k) x[k] = clampr(p[k] - q[k], A.clamp);
-        }
-    }
-    Real out[D];
-    c2v_rule<D>(x, d, flip, A.clamp, A.sat, out);
-#pragma unroll
-    for (int k = 0; k < D; ++k) st_if(c2v_row + k * 32, out[k], live && k < d);
-}
-
-// Variable phase, regular column degree DV, NV variables per warp pass
-// (independent load streams in flight): joint posterior prior + sum of every
-// matrix's c2v in ascending edge order (posterior_pass, _kernels.py:293-301),
-// hard decision post < 0 (ties -> 0) as a ballot (hard_pass).  Edge slots,
-// noisy words and previous hard words come from the chunk's shared stage.
-template <class Real, int DV, int NV>
-__device__ __forceinline__ void var_items_regular(const DecodeArgs<Real>& A, int g, int i0, int nv, int t,
-                                                  unsigned act, int lane, const int* sedge, int sstride,
-                                                  const unsigned* snoisy, const unsigned* sold, Real L)
-{
-    const bool live = (act >> lane) & 1u;
-    const Real* c2vg = A.c2v + (size_t)g * A.slots * 32 + lane;
-    Real c[NV][DV];
-#pragma unroll
-    for (int v = 0; v < NV; ++v)
-#pragma unroll
-        for (int k = 0; k < DV; ++k) {
-            const int e = v < nv ? sedge[v * sstride + k] : 0;
-            c[v][k] = ld_cg_if(c2vg + (unsigned)e * 32u, live && v < nv);
-        }
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-        if (v >= nv) break;
-        const int i = i0 + v;
-        Real acc = ((snoisy[v] >> lane) & 1u) ? -L : L;
-#pragma unroll
-        for (int k = 0; k < DV; ++k) acc += c[v][k];
-        const size_t w = (size_t)g * A.n + i;
-        st_if(A.post + w * 32 + lane, acc, live);
-        const unsigned neg = __ballot_sync(kFull, acc < Real(0));
-        if (lane == 0) {
-            const unsigned hw = (neg & act) | (sold[v] & ~act);
-            A.hard_w[w] = hw;
-            if (A.hist_w) A.hist_w[((size_t)t * A.G) * A.n + w] = hw;
-        }
-    }
-}
-
-// Variable phase, general degrees (CSR) and isolated-per-matrix mode: also
-// the per-matrix totals v2c_pass uses (_kernels.py:276-279).
-template <class Real, bool ISO>
-__device__ __forceinline__ void var_item(const DecodeArgs<Real>& A, int g, int i, int t,
-                                         unsigned act, int lane)
-{
-    const int p0 = A.dv ? i * A.dv : ld_ro(A.var_ptr + i);
-    const int dv = A.dv ? A.dv : ld_ro(A.var_ptr + i + 1) - p0;
-    const bool live = (act >> lane) & 1u;
-    const size_t w = (size_t)g * A.n + i;
-    const unsigned nwd = ld_ro(A.noisy_w + w);
-    const unsigned old = lane == 0 ? ld_cg(A.hard_w + w) : 0u;
-    const Real L = ld_ro(A.Lmag + g * 32 + lane);
-    const Real prior = ((nwd >> lane) & 1u) ? -L : L;
-    const Real* c2vg = A.c2v + (size_t)g * A.slots * 32 + lane;
-    Real acc = prior;
-    if (!ISO) {
-        for (int base = 0; base < dv; base += 32) {
-            const int eid = base + lane < dv ? ld_ro(A.var_edge + p0 + base + lane) : 0;
-            const int cnt = min(32, dv - base);
-#pragma unroll 4
-            for (int k = 0; k < cnt; ++k) {
-                const int e = __shfl_sync(kFull, eid, k);
-                acc += ld_cg_if(c2vg + (size_t)e * 32, live);
-            }
-        }
-        st_if(A.post + w * 32 + lane, acc, live);
-    } else {
-        const size_t P = (size_t)(A.u + 1);
-        Real part = prior;
-        int l = 0;
-        for (int base = 0; base < dv; base += 32) {
-            const int eid = base + lane < dv ? ld_ro(A.var_edge + p0 + base + lane) : 0;
-            const int cnt = min(32, dv - base);
-            for (int k = 0; k < cnt; ++k) {
-                const int e = __shfl_sync(kFull, eid, k);
-                while (e >= A.edge_off[l + 1]) {  // close the totals of matrices before e's
-                    st_if(A.post + (((size_t)g * P + l) * A.n + i) * 32 + lane, part, live);
-                    part = prior;
-                    ++l;
-                }
-                const Real cv = ld_cg_if(c2vg + (size_t)e * 32, live);
-                acc += cv;
-                part += cv;
-            }
-        }
-        for (; l < A.u; ++l) {
-            st_if(A.post + (((size_t)g * P + l) * A.n + i) * 32 + lane, part, live);
-            part = prior;
-        }
-        st_if(A.post + (((size_t)g * P + A.u) * A.n + i) * 32 + lane, acc, live);
-    }
-    const unsigned neg = __ballot_sync(kFull, acc < Real(0));
-    if (lane == 0) {
-        const unsigned hw = (neg & act) | (old & ~act);
-        A.hard_w[w] = hw;
-        if (A.hist_w) A.hist_w[((size_t)t * A.G) * A.n + w] = hw;
-    }
-}
-
-// Syndrome phase item: 32 consecutive checks (lane = check) of group g.
-// Mismatch words (bit f = frame f) are turned into per-frame counts with 32
-// ballots and added to cnt[t&1].
-template <class Real>
-__device__ __forceinline__ void syncheck_item(const DecodeArgs<Real>& A, int g, int blk, int t,
-                                              unsigned act, int lane)
-{
-    const int j = blk * 32 + lane;
-    unsigned mism = 0;
-    if (j < A.C) {
-        const unsigned* hw = A.hard_w + (size_t)g * A.n;
-        const int d = ld_ro(A.deg + j);
-        const int* row = A.chk_ell + j * A.Ds;
-        unsigned par = 0;
-        for (int k = 0; k < d; ++k) par ^= ld_cg(hw + ld_ro(row + k));
-        mism = (par ^ ld_ro(A.syn_w + (size_t)g * A.C + j)) & act;
-    }
-    int c = 0;
-#pragma unroll
-    for (int f = 0; f < 32; ++f) {
-        const int pc = __popc(__ballot_sync(kFull, (mism >> f) & 1u));
-        if (lane == f) c = pc;
-    }
-    if (c) atomicAdd(A.cnt + (t & 1) * A.G * 32 + g * 32 + lane, c);
-    if (__any_sync(kFull, c != 0) && lane == 0) atomicOr(A.any_bad + (t & 1), 1);
-}
-
-__device__ __forceinline__ unsigned long long globaltimer()
-{
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-
-template <class Real>
-__device__ __forceinline__ void stamp(const DecodeArgs<Real>& A, int& k)
-{
-    if (A.ts && blockIdx.x == 0 && threadIdx.x == 0 && k < A.ts_cap) A.ts[k] = globaltimer();
-    ++k;
-}
-
-// Dynamic work distribution: warps claim chunks of consecutive items from a
-// per-phase counter (balanced tails); a chunk's graph rows and per-item words
-// are staged in the warp's shared-memory slice with one coalesced load.
-template <int D> struct Chunk {
-    static constexpr int CH = D <= 16 ? 32 : 8;   // items per claim (check / variable phases)
-    static constexpr int SD = D | 1;               // odd smem row stride: conflict-free staging
-};
-constexpr int kSynChunk = 16;                      // syndrome-phase items (32 checks each)
-
-// items per claim: CH for large phases, fewer when a phase has less than
-// ~4 chunks per warp (small batches), so all warps get work
-__device__ __forceinline__ int chunk_size(int total, int nwarps, int CH)
-{
-    return max(1, min(CH, total / (4 * nwarps)));
-}
-
-__device__ __forceinline__ int claim(unsigned* counter, int lane, int n)
-{
-    unsigned base = 0;
-    if (lane == 0) base = atomicAdd(counter, (unsigned)n);
-    return (int)__shfl_sync(kFull, base, 0);
-}
-
-__device__ __forceinline__ unsigned group_mask(const int* cprev, int g, int lane)
-{
-    return __ballot_sync(kFull, ld_cg(cprev + g * 32 + lane) != 0);
-}
-
-// one claimed chunk of the check phase: items [base, end) of the G*C space
-template <class Real, int D, bool DAMP, bool ISO>
-__device__ __forceinline__ void check_chunk(const DecodeArgs<Real>& A, int base, int end, int t,
-                                            const int* cprev, int lane, int* s_idx, unsigned* s_w,
-                                            int* s_d)
-{
-    constexpr int SD = Chunk<D>::SD;
-    const int rows = end - base;
-    if (lane < rows) {
-        const int item = base + lane;
-        const int j = item % A.C;
-        const int d = ld_ro(A.deg + j);
-        s_d[lane] = d;
-        s_w[lane] = ld_ro(A.syn_w + item);  // syn_w index == item (g*C + j)
-        const int* row = A.chk_ell + j * A.Ds;
-#pragma unroll
-        for (int k = 0; k < D; ++k)
-            if (k < d) s_idx[lane * SD + k] = ld_ro(row + k);
-    }
-    __syncwarp();
-    int g = base / A.C;
-    int j = base - g * A.C;
-    unsigned act = group_mask(cprev, g, lane);
-    Real L = ld_ro(A.Lmag + g * 32 + lane);
-    for (int r = 0; r < rows; ++r) {
-        if (act) check_item<Real, D, DAMP, ISO>(A, g, j, t, act, lane, s_idx + r * SD, s_d[r], s_w[r], L);
-        if (++j == A.C && r + 1 < rows) {
-            j = 0;
-            ++g;
-            act = group_mask(cprev, g, lane);
-            L = ld_ro(A.Lmag + g * 32 + lane);
-        }
-    }
-    __syncwarp();
-}
-
-// one claimed chunk of the variable phase (regular column degree DV)
-template <class Real, int DV>
-__device__ __forceinline__ void var_chunk_regular(const DecodeArgs<Real>& A, int base, int end, int t,
-                                                  const int* cprev, int lane, int* s_idx, unsigned* s_w,
-                                                  unsigned* s_old)
-{
-    constexpr int SV = DV | 1;
-    const int rows = end - base;
-    if (lane < rows) {
-        const int item = base + lane;            // == g*n + i
-        const int i = item % A.n;
-        s_w[lane] = ld_ro(A.noisy_w + item);
-        s_old[lane] = ld_cg(A.hard_w + item);
-        const int* row = A.var_edge + i * DV;
-#pragma unroll
-        for (int k = 0; k < DV; ++k) s_idx[lane * SV + k] = ld_ro(row + k);
-    }
-    __syncwarp();
-    int r = 0;
-    while (r < rows) {
-        const int item = base + r;
-        const int g = item / A.n;
-        const int i = item - g * A.n;
-        const int span = min(rows - r, A.n - i);
-        const unsigned act = group_mask(cprev, g, lane);
-        const Real L = ld_ro(A.Lmag + g * 32 + lane);
-        if (act) {
-            for (int k = 0; k < span; k += 2)
-                var_items_regular<Real, DV, 2>(A, g, i + k, min(2, span - k), t, act, lane,
-                                               s_idx + (r + k) * SV, SV, s_w + r + k, s_old + r + k, L);
-        }
-        r += span;
-    }
-    __syncwarp();
-}
-
-#ifndef MBP_FP32_MIN_BLOCKS
-#define MBP_FP32_MIN_BLOCKS 4
-#endif
-template <class Real, int D>
-constexpr int decode_min_blocks() { return (sizeof(Real) == 4 && D <= 16) ? MBP_FP32_MIN_BLOCKS : 2; }
-
-constexpr int kDecodeThreads = 256;
-
-template <class Real, int D, bool DAMP, bool ISO>
-__global__ void __launch_bounds__(kDecodeThreads, decode_min_blocks<Real, D>())
-decode_kernel(const DecodeArgs<Real> A)
-{
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int nthreads = gridDim.x * blockDim.x;
-    const int nwarps = nthreads >> 5;
-    const int F = A.G * 32;
-    const int cblk = (A.C + 31) / 32;
-    constexpr int CH = Chunk<D>::CH;
-    constexpr int SLICE = CH * (Chunk<D>::SD > 9 ? Chunk<D>::SD : 9);   // ints per warp (check or var rows)
-    __shared__ int s_idx_all[kDecodeThreads / 32][SLICE];
-    __shared__ unsigned s_w_all[kDecodeThreads / 32][CH];
-    __shared__ unsigned s_x_all[kDecodeThreads / 32][CH];
-    int* s_idx = s_idx_all[warp];
-    unsigned* s_w = s_w_all[warp];
-    unsigned* s_x = s_x_all[warp];
-    int ts_k = 0;
-    int wc = 0;  // next work counter
-    stamp(A, ts_k);
-
-    // iteration 0: the uncorrected key against all u*m syndromes (_kernels.py:358-365)
-    {
-        const int total = A.G * cblk;
-        for (int base = claim(A.work + wc, lane, kSynChunk); base < total;
-             base = claim(A.work + wc, lane, kSynChunk))
-            for (int item = base; item < min(base + kSynChunk, total); ++item)
-                syncheck_item<Real>(A, item / cblk, item % cblk, 0, kFull, lane);
-        ++wc;
-    }
-
-    int t = 1;
-    int final_t = 0;
-    for (;; ++t) {
-        grid_barrier(A.barrier);
-        stamp(A, ts_k);
-        const int* cprev = A.cnt + ((t - 1) & 1) * F;
-        // frames whose sweep t-1 decision satisfied every syndrome stop here
-        for (int f = gtid; f < F; f += nthreads) {
-            if (ld_cg(cprev + f) == 0 && A.iters[f] < 0) A.iters[f] = t - 1;
-            A.cnt[(t & 1) * F + f] = 0;
-        }
-        if (ld_cg(A.any_bad + ((t - 1) & 1)) == 0 || t > A.max_it) {
-            final_t = t - 1;
-            break;
-        }
-        if (gtid == 0) A.any_bad[t & 1] = 0;
-
-        {   // check phase
-            const int total = A.G * A.C;
-            const int ch = chunk_size(total, nwarps, CH);
-            for (int base = claim(A.work + wc, lane, ch); base < total; base = claim(A.work + wc, lane, ch))
-                check_chunk<Real, D, DAMP, ISO>(A, base, min(base + ch, total), t, cprev, lane,
-                                                s_idx, s_w, reinterpret_cast<int*>(s_x));
-            ++wc;
-        }
-        grid_barrier(A.barrier);
-        stamp(A, ts_k);
-        {   // variable phase
-            const int total = A.G * A.n;
-            const int ch = chunk_size(total, nwarps, CH);
-            for (int base = claim(A.work + wc, lane, ch); base < total; base = claim(A.work + wc, lane, ch)) {
-                const int end = min(base + ch, total);
-                if (!ISO && A.dv == 6) {
-                    var_chunk_regular<Real, 6>(A, base, end, t, cprev, lane, s_idx, s_w, s_x);
-                } else if (!ISO && A.dv == 9) {
-                    var_chunk_regular<Real, 9>(A, base, end, t, cprev, lane, s_idx, s_w, s_x);
-                } else {
-                    int item = base;
-                    while (item < end) {
-                        const int g = item / A.n;
-                        const int i = item - g * A.n;
-                        const unsigned act = group_mask(cprev, g, lane);
-                        const int span = min(end - item, A.n - i);
-                        if (act)
-                            for (int k = 0; k < span; ++k) var_item<Real, ISO>(A, g, i + k, t, act, lane);
-                        item += span;
-                    }
-                }
-            }
-            ++wc;
-        }
-        grid_barrier(A.barrier);
-        stamp(A, ts_k);
-        {   // syndrome phase
-            const int total = A.G * cblk;
-            for (int base = claim(A.work + wc, lane, kSynChunk); base < total;
-                 base = claim(A.work + wc, lane, kSynChunk)) {
-                const int end = min(base + kSynChunk, total);
-                int g = base / cblk;
-                unsigned act = group_mask(cprev, g, lane);
-                for (int item = base; item < end; ++item) {
-                    const int gi = item / cblk;
-                    if (gi != g) { g = gi; act = group_mask(cprev, g, lane); }
-                    if (act) syncheck_item<Real>(A, g, item - g * cblk, t, act, lane);
-                }
-            }
-            ++wc;
-        }
-    }
-
-    // per-frame results (DecodeResult fields, decoder.py:246-274)
-    const int* cfin = A.cnt + (final_t & 1) * F;
-    for (int f = gtid; f < A.B; f += nthreads) {
-        const int c = ld_cg(cfin + f);
-        const int it = A.iters[f];
-        const bool conv = it >= 0;
-        A.out_conv[f] = conv ? 1 : 0;
-        A.out_iters[f] = conv ? it : A.max_it;
-        A.out_mism[f] = conv ? 0 : c;
-    }
-    if (gtid == 0) *A.sweeps_run = final_t;
-    stamp(A, ts_k);
-}
+constexpr int kDecodeThreads = 256;  // decode kernel block size (decode.cuh)
 
 // ---------------------------------------------------------------------------
 // bit-matrix transposes between BitBlock rows and 32-frame words

@@ -5,7 +5,7 @@
 // cooperative decode kernel of kernels.cuh.  No torch, no Python: callers
 // bind it with ctypes (paper_2001_07979_b200/_native.py) or any FFI.
 #include "../../include/mbp.h"
-#include "kernels.cuh"
+#include "decode.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -103,8 +103,10 @@ struct mbp_workspace {
     int cap = 0, G = 0;
     size_t real_size = 4;
     DevBuf c2v, post, v2c, Lmag, noisy_w, syn_w, hard_w, hist_w, cnt, any_bad, iters, barrier,
-        sweeps, ts, work, tmp_in, tmp_out, tmp_conv, tmp_iters, tmp_mism, tmp_e;
+        sweeps, ts, work, tmp_in,
+        c2v_b, post_b, v2c_b, Lmag_b, noisy_b, syn_b, hard_b, cnt_b, fid_b, src_b, newslot, grp_cnt, ctrl, tmp_out, tmp_conv, tmp_iters, tmp_mism, tmp_e;
     int ts_cap = 0;
+    int Gb = 0;        // compaction capacity (groups), 0 = disabled
     cudaStream_t own_stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
     int last_B = 0;
@@ -268,15 +270,38 @@ static int ws_alloc(mbp_workspace* ws)
     const size_t hist_bytes = (ws->cfg.flags & MBP_RECORD_HISTORY)
         ? (size_t)(ws->cfg.max_iterations + 1) * ws->G * ens->n * 4 : 0;
     if (ws->hist_w.bytes != hist_bytes && (rc = ws->hist_w.alloc(hist_bytes))) return rc;
+    // frame compaction (decode.cuh): secondary layout of ceil(G/2) groups;
+    // off for the diagnostic modes, which read state by original frame index
+    const bool compaction = ws->G >= 2 && !(ws->cfg.flags & (MBP_RECORD_HISTORY | MBP_KEEP_STATE | MBP_NO_COMPACTION));
+    ws->Gb = compaction ? (ws->G + 1) / 2 : 0;
+    {
+        const size_t Gb = ws->Gb, Fb = Gb * 32;
+        if (ws->c2v_b.bytes != Gb * slots * 32 * R && (rc = ws->c2v_b.alloc(Gb * slots * 32 * R))) return rc;
+        if (ws->post_b.bytes != Gb * P * ens->n * 32 * R && (rc = ws->post_b.alloc(Gb * P * ens->n * 32 * R))) return rc;
+        const size_t vb = ws->cfg.damping != 0.0 ? Gb * slots * 32 * R : 0;
+        if (ws->v2c_b.bytes != vb && (rc = ws->v2c_b.alloc(vb))) return rc;
+        if (ws->Lmag_b.bytes != Fb * R && (rc = ws->Lmag_b.alloc(Fb * R))) return rc;
+        if (ws->noisy_b.bytes != Gb * ens->n * 4 && (rc = ws->noisy_b.alloc(Gb * ens->n * 4))) return rc;
+        if (ws->hard_b.bytes != Gb * ens->n * 4 && (rc = ws->hard_b.alloc(Gb * ens->n * 4))) return rc;
+        if (ws->syn_b.bytes != Gb * ens->C * 4 && (rc = ws->syn_b.alloc(Gb * ens->C * 4))) return rc;
+        if (ws->cnt_b.bytes != 2 * Fb * 4 && (rc = ws->cnt_b.alloc(2 * Fb * 4))) return rc;
+        if (ws->fid_b.bytes != Fb * 4 && (rc = ws->fid_b.alloc(Fb * 4))) return rc;
+        if (ws->src_b.bytes != Fb * 4 && (rc = ws->src_b.alloc(Fb * 4))) return rc;
+        const size_t F = (size_t)ws->G * 32;
+        if (ws->newslot.bytes != (Gb ? F * 4 : 0) && (rc = ws->newslot.alloc(Gb ? F * 4 : 0))) return rc;
+        if (ws->grp_cnt.bytes != (Gb ? (size_t)ws->G * 4 : 0) && (rc = ws->grp_cnt.alloc(Gb ? (size_t)ws->G * 4 : 0))) return rc;
+        const size_t cb = (size_t)(2 * (ws->cfg.max_iterations + 2)) * 4;
+        if (ws->ctrl.bytes != cb && (rc = ws->ctrl.alloc(cb))) return rc;
+    }
     const size_t work_bytes = (size_t)(3 * (ws->cfg.max_iterations + 1) + 2) * 4;
     if (ws->work.bytes != work_bytes && (rc = ws->work.alloc(work_bytes))) return rc;
-    ws->ts_cap = (ws->cfg.flags & MBP_PROFILE_PHASES) ? 3 * (ws->cfg.max_iterations + 1) + 4 : 0;
+    ws->ts_cap = (ws->cfg.flags & MBP_PROFILE_PHASES) ? 3 * (ws->cfg.max_iterations + 1) + 8 : 0;
     if (ws->ts.bytes != (size_t)ws->ts_cap * 8 && (rc = ws->ts.alloc((size_t)ws->ts_cap * 8))) return rc;
     if (!ws->Lmag.p) {
         if ((rc = ws->Lmag.alloc(F * R)) || (rc = ws->noisy_w.alloc((size_t)ws->G * ens->n * 4)) ||
             (rc = ws->syn_w.alloc((size_t)ws->G * ens->C * 4)) || (rc = ws->hard_w.alloc((size_t)ws->G * ens->n * 4)) ||
             (rc = ws->cnt.alloc(2 * F * 4)) || (rc = ws->any_bad.alloc(2 * 4)) || (rc = ws->iters.alloc(F * 4)) ||
-            (rc = ws->barrier.alloc(2 * 4)) || (rc = ws->sweeps.alloc(4)))
+            (rc = ws->barrier.alloc(2 * 4)) || (rc = ws->sweeps.alloc(2 * 4)))
             return rc;
     }
     return MBP_OK;
@@ -474,6 +499,13 @@ static int decode_chunk(mbp_workspace* ws, const uint8_t* noisy, const uint8_t* 
     MBP_CUDA(cudaMemsetAsync(ws->iters.p, 0xff, (size_t)F * 4, s));
     MBP_CUDA(cudaMemsetAsync(ws->barrier.p, 0, 8, s));
     MBP_CUDA(cudaMemsetAsync(ws->work.p, 0, ws->work.bytes, s));
+    MBP_CUDA(cudaMemsetAsync(ws->sweeps.p, 0, 8, s));
+    if (ws->Gb) {
+        MBP_CUDA(cudaMemsetAsync(ws->ctrl.p, 0, ws->ctrl.bytes, s));
+        MBP_CUDA(cudaMemsetAsync(ws->fid_b.p, 0xff, ws->fid_b.bytes, s));
+        MBP_CUDA(cudaMemsetAsync(ws->src_b.p, 0xff, ws->src_b.bytes, s));
+        MBP_CUDA(cudaMemsetAsync(ws->newslot.p, 0xff, ws->newslot.bytes, s));
+    }
 
     mbp::DecodeArgs<Real> A;
     std::memset(&A, 0, sizeof A);
@@ -490,6 +522,13 @@ static int decode_chunk(mbp_workspace* ws, const uint8_t* noisy, const uint8_t* 
     A.noisy_w = ws->noisy_w.as<unsigned>(); A.syn_w = ws->syn_w.as<unsigned>();
     A.hard_w = ws->hard_w.as<unsigned>(); A.hist_w = record ? ws->hist_w.as<unsigned>() : nullptr;
     A.cnt = ws->cnt.as<int>(); A.any_bad = ws->any_bad.as<int>(); A.iters = ws->iters.as<int>();
+    // compaction only pays when the chunk has at least two groups
+    A.Gb = G >= 2 ? std::min(ws->Gb, (G + 1) / 2) : 0;
+    A.c2v_b = ws->c2v_b.as<Real>(); A.post_b = ws->post_b.as<Real>(); A.v2c_b = ws->v2c_b.as<Real>();
+    A.Lmag_b = ws->Lmag_b.as<Real>(); A.noisy_b = ws->noisy_b.as<unsigned>(); A.syn_b = ws->syn_b.as<unsigned>();
+    A.hard_b = ws->hard_b.as<unsigned>(); A.cnt_b = ws->cnt_b.as<int>(); A.fid_b = ws->fid_b.as<int>();
+    A.src_b = ws->src_b.as<int>(); A.newslot = ws->newslot.as<int>(); A.grp_cnt = ws->grp_cnt.as<int>();
+    A.ctrl = ws->ctrl.as<int>();
     A.barrier = ws->barrier.as<unsigned>(); A.work = ws->work.as<unsigned>(); A.sweeps_run = ws->sweeps.as<int>();
     A.ts = ws->ts_cap ? ws->ts.as<unsigned long long>() : nullptr; A.ts_cap = ws->ts_cap;
     A.B = B; A.out_conv = conv; A.out_iters = iters; A.out_mism = mism;
@@ -706,9 +745,23 @@ int mbp_workspace_read_phase_times(mbp_workspace* ws, uint64_t* ns, int32_t cap,
     int sweeps = 0;
     MBP_CUDA(cudaMemcpy(&sweeps, ws->sweeps.p, 4, cudaMemcpyDeviceToHost));
     // stamps: start, 3 per executed sweep, the final check's barrier, end
-    const int k = std::min(ws->ts_cap, 3 * sweeps + 3);
+    const int k = std::min(ws->ts_cap - 4, 3 * sweeps + 3);
     *count = k;
     MBP_CUDA(cudaMemcpy(ns, ws->ts.p, (size_t)std::min(k, cap) * 8, cudaMemcpyDeviceToHost));
+    // the last 4 slots: compaction stamps (start, maps built, moved, done)
+    if (cap >= k + 4) MBP_CUDA(cudaMemcpy(ns + k, ws->ts.as<char>() + (size_t)(ws->ts_cap - 4) * 8, 32, cudaMemcpyDeviceToHost));
+    return MBP_OK;
+}
+
+int mbp_workspace_last_stats(mbp_workspace* ws, int32_t* sweeps, int32_t* compaction_sweep)
+{
+    if (!ws) return fail(MBP_EINVAL, "workspace is null");
+    DeviceGuard dg(ws->ens->device);
+    int v[2] = {0, 0};
+    MBP_CUDA(cudaDeviceSynchronize());
+    MBP_CUDA(cudaMemcpy(v, ws->sweeps.p, 8, cudaMemcpyDeviceToHost));
+    if (sweeps) *sweeps = v[0];
+    if (compaction_sweep) *compaction_sweep = v[1];
     return MBP_OK;
 }
 

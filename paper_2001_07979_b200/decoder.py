@@ -292,11 +292,13 @@ class BatchDecoder:
         """Per-phase device time (ms) of the last decode chunk
         (needs flags MBP_PROFILE_PHASES): check / variable / syndrome phase
         totals over the executed sweeps, the initial check and the tail."""
-        cap = 3 * (self.config.max_iterations + 1) + 4
+        cap = 3 * (self.config.max_iterations + 1) + 8
         buf = np.zeros(cap, dtype=np.uint64)
         cnt = C.c_int32(0)
         N.call("mbp_workspace_read_phase_times", self.handle, buf.ctypes.data, cap, C.byref(cnt))
-        ts = buf[: min(cnt.value, cap)].astype(np.float64) / 1e6
+        k = min(cnt.value, cap - 4)
+        ts = buf[:k].astype(np.float64) / 1e6
+        cts = buf[k:k + 4].astype(np.float64) / 1e6
         d = np.diff(ts)
         sweeps = (len(ts) - 3) // 3
         out = {"sweeps": sweeps, "total_ms": float(ts[-1] - ts[0]), "syncheck0_ms": float(d[0])}
@@ -304,7 +306,17 @@ class BatchDecoder:
             body = d[1:1 + 3 * sweeps].reshape(sweeps, 3)
             out.update(check_ms=body[:, 0].tolist(), var_ms=body[:, 1].tolist(), syncheck_ms=body[:, 2].tolist())
         out["tail_ms"] = float(d[-1]) if len(d) > 1 else 0.0
+        if cts[0] > 0:
+            cd = np.diff(cts)
+            out["compaction_ms"] = {"maps": float(cd[0]), "move": float(cd[1]), "barrier": float(cd[2])}
         return out
+
+    def last_stats(self):
+        """(sweeps run, sweep at which frames were compacted or 0) of the last chunk."""
+        sw = C.c_int32(0)
+        cs = C.c_int32(0)
+        N.call("mbp_workspace_last_stats", self.handle, C.byref(sw), C.byref(cs))
+        return int(sw.value), int(cs.value)
 
     def last_timing(self, e2e: bool = False):
         """(decode-kernel ms, sweeps run) of the last decode; with e2e=True

@@ -323,3 +323,37 @@ def test_device_tensor_path(golden_cfg1, cfg1_ensemble):
     assert np.array_equal(corrected.cpu().numpy()[g["e070_converged"]], g["e070_corrected"][g["e070_converged"]])
     keys = torch.from_numpy(g["e070_key"]).to(dev)
     assert np.array_equal(dec.syndromes(keys).cpu().numpy(), g["e070_syn"])
+
+
+# ---------------------------------------------------------------------------
+# frame compaction (decode.cuh) must be invisible in every output
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("variant", ["default", "damp25", "isolated", "fp64"])
+def test_compaction_is_transparent(golden_mid, mid_ensemble, cfg1_ensemble, variant):
+    cfgs = {"default": DecoderConfig(), "damp25": DecoderConfig(damping=0.25),
+            "isolated": DecoderConfig(combining_mode="isolated-per-matrix"),
+            "fp64": DecoderConfig(precision="fp64")}
+    cfg = cfgs[variant]
+    cases = []
+    # mixed easy/hard frames: mid ensemble u=1 (failures run to the limit) and cfg1 at e=0.09
+    g = golden_mid
+    noisy = np.concatenate([g[f"default_e{e}_u1_noisy"] for e in ("050", "080", "110")])
+    syn = np.concatenate([g[f"default_e{e}_u1_syn"] for e in ("050", "080", "110")])
+    cases.append((mid_ensemble.prefix(1), noisy, syn, np.repeat([0.05, 0.08, 0.11], 12)))
+    fb = make_frames(cfg1_ensemble.n, 0.09, 320, seed=11)
+    dec0 = BatchDecoder(cfg1_ensemble, 320)
+    cases.append((cfg1_ensemble, fb.noisy, dec0.syndromes(fb.keys), 0.09))
+    compacted = 0
+    for ens, nz, sy, e in cases:
+        on = BatchDecoder(ens, nz.shape[0], cfg)
+        off = BatchDecoder(ens, nz.shape[0], cfg, flags=N.MBP_NO_COMPACTION)
+        a = on.decode(nz, sy, e)
+        compacted += on.last_stats()[1] > 0
+        b = off.decode(nz, sy, e)
+        assert off.last_stats()[1] == 0
+        assert np.array_equal(a.corrected, b.corrected)
+        assert np.array_equal(a.converged, b.converged)
+        assert np.array_equal(a.iterations, b.iterations)
+        assert np.array_equal(a.mismatches, b.mismatches)
+    assert compacted >= 1

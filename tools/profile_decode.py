@@ -28,12 +28,13 @@ def main():
     ap.add_argument("--precision", default="fp32")
     ap.add_argument("--once", action="store_true")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--no-compact", action="store_true")
     a = ap.parse_args()
     import torch
 
     ens = load_ensemble(next((ROOT / "paper_2001_07979_b200" / "ensembles").glob(f"{a.cfg}_*.npz")))
     fb = make_frames(ens.n, a.e, a.frames, seed=0)
-    flags = 0 if a.once else N.MBP_PROFILE_PHASES
+    flags = (0 if a.once else N.MBP_PROFILE_PHASES) | (N.MBP_NO_COMPACTION if a.no_compact else 0)
     dec = BatchDecoder(ens, a.frames, DecoderConfig(precision=a.precision), flags=flags)
     dev = torch.device("cuda:0")
     keys = torch.from_numpy(fb.keys).to(dev)
@@ -49,7 +50,7 @@ def main():
         dec.decode_device(noisy, syn, e, out=out)
         torch.cuda.synchronize()
         kms, sweeps = dec.last_timing()
-        res.append({"kernel_ms": kms, **dec.phase_times()})
+        res.append({"kernel_ms": kms, "compaction_sweep": dec.last_stats()[1], **dec.phase_times()})
     it = out[2].cpu().numpy()
     ok = out[1].cpu().numpy().astype(bool) & np.all(out[0].cpu().numpy() == fb.keys, axis=1)
     print(json.dumps({"cfg": a.cfg, "frames": a.frames, "e": a.e, "precision": a.precision,
