@@ -65,7 +65,10 @@ enum {
     MBP_RECORD_HISTORY = 1,  /* keep the hard decision after every sweep     */
     MBP_KEEP_STATE = 2,      /* keep posteriors/messages readable after decode */
     MBP_PROFILE_PHASES = 4,  /* record a globaltimer stamp at every phase barrier */
-    MBP_NO_COMPACTION = 8    /* never repack undecided frames into dense groups   */
+    MBP_NO_COMPACTION = 8,   /* never repack undecided frames into dense groups   */
+    MBP_EXPLICIT_MESSAGES = 16 /* fp32 joint undamped runs: use the explicit-message
+                                  kernel (every c2v stored) instead of the scatter
+                                  kernel; needed to read c2v back                 */
 };
 
 typedef struct mbp_decoder_config {

@@ -17,6 +17,7 @@ MBP_OK, MBP_EINVAL, MBP_ECUDA, MBP_EUNSUPPORTED, MBP_ENOMEM = range(5)
 MBP_JOINT_GRAPH, MBP_ISOLATED_PER_MATRIX = 0, 1
 MBP_FP32_PHI, MBP_FP64_TANH = 0, 1
 MBP_RECORD_HISTORY, MBP_KEEP_STATE, MBP_PROFILE_PHASES, MBP_NO_COMPACTION = 1, 2, 4, 8
+MBP_EXPLICIT_MESSAGES = 16
 
 #: every symbol include/mbp.h declares (checked by tests/test_native_abi.py)
 EXPORTS = (

@@ -2,8 +2,10 @@
 
     python -m paper_2001_07979_b200.build [--force]
 
-The shared library lands in paper_2001_07979_b200/_lib/ (git-ignored, but it
-travels to the GPU box with the gpurun snapshot).  cudart is linked
+The kernel template instances are split over several translation units
+(csrc/k_*.cu) that compile in parallel; mbp.cu holds the host code and the
+C ABI.  The shared library lands in paper_2001_07979_b200/_lib/ (git-ignored,
+but it travels to the GPU box with the gpurun snapshot).  cudart is linked
 statically so the .so depends only on the driver.
 """
 
@@ -13,23 +15,28 @@ import os
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
+OBJ_DIR = LIB_DIR / "obj"
 LIB = LIB_DIR / "libmbp_b200.so"
-SOURCES = [CSRC / "mbp.cu"]
-DEPS = SOURCES + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "mbp.h"]
-
-NVCC_FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
-    "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC,-O2",
-    "-shared", "-cudart", "static",
-    "-I", str(ROOT / "include"),
+# (object name, source, extra defines)
+UNITS = [
+    ("mbp", "mbp.cu", []),
+    ("k_explicit_f32", "k_explicit.cu", []),
+    ("k_explicit_f64", "k_explicit.cu", ["-DMBP_EXPLICIT_F64"]),
+    ("k_scatter_0", "k_scatter.cu", ["-DMBP_SCATTER_PART=0"]),
+    ("k_scatter_1", "k_scatter.cu", ["-DMBP_SCATTER_PART=1"]),
+    ("k_scatter_2", "k_scatter.cu", ["-DMBP_SCATTER_PART=2"]),
 ]
+DEPS = sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [ROOT / "include" / "mbp.h"]
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-I", str(ROOT / "include")]
 
 
 def nvcc() -> str:
@@ -46,12 +53,30 @@ def stale() -> bool:
     return any(p.stat().st_mtime > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) -> Path:
     if not force and not stale():
         return LIB
-    LIB_DIR.mkdir(parents=True, exist_ok=True)
+    OBJ_DIR.mkdir(parents=True, exist_ok=True)
+    cc = nvcc()
+
+    def compile_unit(unit):
+        name, src, defs = unit
+        obj = OBJ_DIR / f"{name}.o"
+        cmd = [cc, *NVCC_FLAGS, *defs, *(["-Xptxas", "-v"] if ptxas_info else []), "-c", "-o", str(obj),
+               str(CSRC / src)]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src} {defs}:\n{r.stderr}")
+        if ptxas_info or verbose:
+            sys.stderr.write(r.stderr)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(UNITS)) as pool:
+        objs = list(pool.map(compile_unit, UNITS))
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(tmp), *map(str, SOURCES)]
+    cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
@@ -60,4 +85,4 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, ptxas_info="--ptxas" in sys.argv))

@@ -319,14 +319,14 @@ __device__ __forceinline__ unsigned long long globaltimer()
 }
 
 // compaction stamps live in the last 4 timestamp slots
-template <class Real>
-__device__ __forceinline__ void stamp_compact(const DecodeArgs<Real>& A, int k)
+template <class Args>
+__device__ __forceinline__ void stamp_compact(const Args& A, int k)
 {
     if (A.ts && blockIdx.x == 0 && threadIdx.x == 0 && A.ts_cap >= 8) A.ts[A.ts_cap - 4 + k] = globaltimer();
 }
 
-template <class Real>
-__device__ __forceinline__ void stamp(const DecodeArgs<Real>& A, int& k)
+template <class Args>
+__device__ __forceinline__ void stamp(const Args& A, int& k)
 {
     if (A.ts && blockIdx.x == 0 && threadIdx.x == 0 && k < A.ts_cap) A.ts[k] = globaltimer();
     ++k;
@@ -567,8 +567,8 @@ __device__ __forceinline__ int compact(const DecodeArgs<Real>& A, int t, int gw,
 // into the primary hard_w (original layout) for the row transpose.  Warp item
 // = 32 consecutive words of one original group (lane = word); the group's
 // moved frames (a few) are walked one by one with coalesced word loads.
-template <class Real>
-__device__ __forceinline__ void scatter_back(const DecodeArgs<Real>& A, int gw, int nw, int lane)
+template <class Args>
+__device__ __forceinline__ void scatter_back(const Args& A, int gw, int nw, int lane)
 {
     const int xchunks = (A.n + 31) / 32;
     for (long long it = gw; it < (long long)A.G * xchunks; it += nw) {
@@ -771,7 +771,7 @@ decode_kernel(const DecodeArgs<Real> A)
         A.out_iters[f] = conv ? it : A.max_it;
         A.out_mism[f] = conv ? 0 : c;
     }
-    if (cpt) scatter_back<Real>(A, gw, nwarps, lane);
+    if (cpt) scatter_back(A, gw, nwarps, lane);
     if (gtid == 0) A.sweeps_run[0] = final_t;
     stamp(A, ts_k);
 }

@@ -239,7 +239,7 @@ __device__ __forceinline__ unsigned warp_transpose32(unsigned x, int lane)
 
 // rows [B][row_bytes], bits [seg_off*8 + 32c, +32) of segment s of each row ->
 // words[g][word_off + 32c + lane].  grid-stride over (g, segment, chunk).
-__global__ void rows_to_words_kernel(const uint8_t* __restrict__ rows, long long row_bytes, int B,
+static __global__ void rows_to_words_kernel(const uint8_t* __restrict__ rows, long long row_bytes, int B,
                                      int G, int nseg, int seg_bits, long long seg_bytes,
                                      unsigned* __restrict__ words, unsigned* __restrict__ words2,
                                      long long words_per_group)
@@ -266,7 +266,7 @@ __global__ void rows_to_words_kernel(const uint8_t* __restrict__ rows, long long
 }
 
 // words[g][word_off + 32c + lane] -> rows (inverse of rows_to_words_kernel)
-__global__ void words_to_rows_kernel(const unsigned* __restrict__ words, long long words_per_group,
+static __global__ void words_to_rows_kernel(const unsigned* __restrict__ words, long long words_per_group,
                                      int B, int G, int nseg, int seg_bits, long long seg_bytes,
                                      uint8_t* __restrict__ rows, long long row_bytes)
 {
@@ -293,7 +293,7 @@ __global__ void words_to_rows_kernel(const unsigned* __restrict__ words, long lo
 
 // Alice side, Eq. 1: syndrome words of 32 frames per check, z = XOR of key
 // words over the row (syndrome_pass, _kernels.py:220-227, 32 frames wide).
-__global__ void syndrome_words_kernel(const uint8_t* __restrict__ deg, const int* __restrict__ chk_ell, int D,
+static __global__ void syndrome_words_kernel(const uint8_t* __restrict__ deg, const int* __restrict__ chk_ell, int D,
                                       int n, int C, int G, const unsigned* __restrict__ key_w,
                                       unsigned* __restrict__ syn_w)
 {

@@ -1,0 +1,32 @@
+// launch.h -- kernel launchers shared between mbp.cu (host/C ABI) and the
+// kernel translation units (one per group of template instantiations, so
+// the library builds in parallel).
+#pragma once
+
+#include "scatter.cuh"
+
+namespace mbp {
+
+// Cooperative launch of one persistent decode kernel instance sized to the
+// device (resident blocks per SM x sm_count).  Return cudaErrorNotSupported
+// when no instance exists for the requested degree bound.
+cudaError_t launch_explicit_f32(const DecodeArgs<float>& A, int D, bool damp, bool iso, int sm_count,
+                                cudaStream_t s);
+cudaError_t launch_explicit_f64(const DecodeArgs<double>& A, int D, bool damp, bool iso, int sm_count,
+                                cudaStream_t s);
+cudaError_t launch_scatter_small(const ScatterArgs& A, int D, int sm_count, cudaStream_t s);   // D 3..8
+cudaError_t launch_scatter_mid(const ScatterArgs& A, int D, int sm_count, cudaStream_t s);     // D 9..16
+cudaError_t launch_scatter_large(const ScatterArgs& A, int D, int sm_count, cudaStream_t s);   // D 20..64
+
+template <class Kern, class Args>
+cudaError_t launch_coop(Kern kern, const Args& A, int sm_count, cudaStream_t s)
+{
+    int per_sm = 0;
+    cudaError_t err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDecodeThreads, 0);
+    if (err != cudaSuccess) return err;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    void* args[] = {(void*)&A};
+    return cudaLaunchCooperativeKernel((const void*)kern, dim3(per_sm * sm_count), dim3(kDecodeThreads), args, 0, s);
+}
+
+}  // namespace mbp

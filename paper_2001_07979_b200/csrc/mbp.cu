@@ -5,7 +5,7 @@
 // cooperative decode kernel of kernels.cuh.  No torch, no Python: callers
 // bind it with ctypes (paper_2001_07979_b200/_native.py) or any FFI.
 #include "../../include/mbp.h"
-#include "decode.cuh"
+#include "launch.h"
 
 #include <algorithm>
 #include <cmath>
@@ -95,6 +95,7 @@ struct mbp_ensemble {
     DevBuf chk_ptr, chk_var, var_ptr, var_edge;  // int32
     // decode layout: padded ELL rows + slot ids per variable
     DevBuf deg, chk_ell, var_slot, ref2slot;
+    DevBuf var_chk;   // stacked check id of each variable's edges (ascending edge order)
 };
 
 struct mbp_workspace {
@@ -105,6 +106,10 @@ struct mbp_workspace {
     DevBuf c2v, post, v2c, Lmag, noisy_w, syn_w, hard_w, hist_w, cnt, any_bad, iters, barrier,
         sweeps, ts, work, tmp_in,
         c2v_b, post_b, v2c_b, Lmag_b, noisy_b, syn_b, hard_b, cnt_b, fid_b, src_b, newslot, grp_cnt, ctrl, tmp_out, tmp_conv, tmp_iters, tmp_mism, tmp_e;
+    // scatter path (scatter.cuh)
+    DevBuf sc_post, sc_acc, sc_mis, sc_Mtab, sc_Lfix, sc_Mfix, sc_Lmax,
+        sc_post_b, sc_acc_b, sc_Mtab_b, sc_Lfix_b, sc_mis_b;
+    bool scatter = false;   // path of the current configuration
     int ts_cap = 0;
     int Gb = 0;        // compaction capacity (groups), 0 = disabled
     cudaStream_t own_stream = nullptr;
@@ -196,6 +201,8 @@ int mbp_ensemble_create(int32_t n, int32_t m, int32_t u, const int64_t* chk_ptr,
         }
     }
     for (long long t = 0; t < E; ++t) vs[t] = r2s[ve[t]];
+    std::vector<int> vchk(E);
+    for (long long t = 0; t < E; ++t) vchk[t] = vs[t] / D;
     int rc;
     {
         DeviceGuard dg(device);
@@ -209,7 +216,8 @@ int mbp_ensemble_create(int32_t n, int32_t m, int32_t u, const int64_t* chk_ptr,
         if ((rc = ens->chk_ptr.alloc(sizeof(int) * (C + 1))) || (rc = ens->chk_var.alloc(sizeof(int) * E)) ||
             (rc = ens->var_ptr.alloc(sizeof(int) * (n + 1))) || (rc = ens->var_edge.alloc(sizeof(int) * E)) ||
             (rc = ens->deg.alloc(C)) || (rc = ens->chk_ell.alloc(sizeof(int) * (size_t)C * D)) ||
-            (rc = ens->var_slot.alloc(sizeof(int) * E)) || (rc = ens->ref2slot.alloc(sizeof(int) * E))) {
+            (rc = ens->var_slot.alloc(sizeof(int) * E)) || (rc = ens->ref2slot.alloc(sizeof(int) * E)) ||
+            (rc = ens->var_chk.alloc(sizeof(int) * E))) {
             delete ens;
             return rc;
         }
@@ -221,6 +229,7 @@ int mbp_ensemble_create(int32_t n, int32_t m, int32_t u, const int64_t* chk_ptr,
         if (err == cudaSuccess) err = cudaMemcpy(ens->chk_ell.p, ell.data(), sizeof(int) * (size_t)C * D, cudaMemcpyHostToDevice);
         if (err == cudaSuccess) err = cudaMemcpy(ens->var_slot.p, vs.data(), sizeof(int) * E, cudaMemcpyHostToDevice);
         if (err == cudaSuccess) err = cudaMemcpy(ens->ref2slot.p, r2s.data(), sizeof(int) * E, cudaMemcpyHostToDevice);
+        if (err == cudaSuccess) err = cudaMemcpy(ens->var_chk.p, vchk.data(), sizeof(int) * E, cudaMemcpyHostToDevice);
         if (err != cudaSuccess) { delete ens; return fail(MBP_ECUDA, std::string("ensemble upload: ") + cudaGetErrorString(err)); }
     }
     *out = ens;
@@ -255,6 +264,29 @@ static int validate_cfg(const mbp_decoder_config* cfg)
     return MBP_OK;
 }
 
+// Degree bound of a scatter-kernel instance (k_scatter.cu), 0 if none.
+static int scatter_degree(int Ds)
+{
+    if (Ds <= 16) return std::max(Ds, 3);
+    for (int d : {20, 24, 32, 48, 64}) if (Ds <= d) return d;
+    return 0;
+}
+
+// The scatter kernel (scatter.cuh) runs fp32, joint-graph, undamped decodes
+// whose fixed-point range stays fine: |acc| <= L + dv_max * clamp must leave
+// >= 19 fractional bits (L <= 745 for any double e).
+static bool scatter_eligible(const mbp_ensemble* ens, const mbp_decoder_config& cfg)
+{
+    return cfg.precision == MBP_FP32_PHI && cfg.combining_mode == MBP_JOINT_GRAPH && cfg.damping == 0.0 &&
+           !(cfg.flags & MBP_EXPLICIT_MESSAGES) && scatter_degree(ens->Ds) != 0 &&
+           (double)ens->dmax_v * cfg.llr_clamp <= 1024.0;
+}
+
+static int fit(DevBuf& b, size_t bytes)
+{
+    return b.bytes == bytes ? MBP_OK : b.alloc(bytes);
+}
+
 // (Re)allocate the buffers whose shape depends on cfg.
 static int ws_alloc(mbp_workspace* ws)
 {
@@ -263,8 +295,10 @@ static int ws_alloc(mbp_workspace* ws)
     const size_t P = ws->cfg.combining_mode == MBP_ISOLATED_PER_MATRIX ? (size_t)ens->u + 1 : 1;
     int rc;
     const size_t slots = (size_t)ens->C * ens->Ds;
+    ws->scatter = scatter_eligible(ens, ws->cfg);
     if (ws->c2v.bytes != ws->G * slots * 32 * R && (rc = ws->c2v.alloc(ws->G * slots * 32 * R))) return rc;
-    if (ws->post.bytes != ws->G * P * ens->n * 32 * R && (rc = ws->post.alloc(ws->G * P * ens->n * 32 * R))) return rc;
+    const size_t post_bytes = ws->scatter ? 0 : ws->G * P * ens->n * 32 * R;
+    if ((rc = fit(ws->post, post_bytes))) return rc;
     const size_t v2c_bytes = ws->cfg.damping != 0.0 ? ws->G * slots * 32 * R : 0;
     if (ws->v2c.bytes != v2c_bytes && (rc = ws->v2c.alloc(v2c_bytes))) return rc;
     const size_t hist_bytes = (ws->cfg.flags & MBP_RECORD_HISTORY)
@@ -292,6 +326,18 @@ static int ws_alloc(mbp_workspace* ws)
         if (ws->grp_cnt.bytes != (Gb ? (size_t)ws->G * 4 : 0) && (rc = ws->grp_cnt.alloc(Gb ? (size_t)ws->G * 4 : 0))) return rc;
         const size_t cb = (size_t)(2 * (ws->cfg.max_iterations + 2)) * 4;
         if (ws->ctrl.bytes != cb && (rc = ws->ctrl.alloc(cb))) return rc;
+    }
+    {   // scatter-path state (sized 0 when the explicit kernel runs)
+        const bool sc = ws->scatter;
+        const size_t G = ws->G, Gb = ws->Gb, n = ens->n, C = ens->C, Dm1 = ens->Ds + 1;
+        if ((rc = fit(ws->sc_post, sc ? 2 * G * n * 32 * 4 : 0)) || (rc = fit(ws->sc_acc, sc ? G * n * 32 * 4 : 0)) ||
+            (rc = fit(ws->sc_mis, sc ? G * C * 4 : 0)) || (rc = fit(ws->sc_Mtab, sc ? Dm1 * G * 32 * 4 : 0)) ||
+            (rc = fit(ws->sc_Lfix, sc ? G * 32 * 4 : 0)) || (rc = fit(ws->sc_Mfix, sc ? Dm1 * G * 32 * 4 : 0)) ||
+            (rc = fit(ws->sc_Lmax, sc ? 4 : 0)) || (rc = fit(ws->sc_post_b, sc ? 2 * Gb * n * 32 * 4 : 0)) ||
+            (rc = fit(ws->sc_acc_b, sc ? Gb * n * 32 * 4 : 0)) || (rc = fit(ws->sc_Mtab_b, sc ? Dm1 * Gb * 32 * 4 : 0)) ||
+            (rc = fit(ws->sc_Lfix_b, sc ? Gb * 32 * 4 : 0)) || (rc = fit(ws->sc_mis_b, sc ? Gb * C * 4 : 0)))
+            return rc;
+        if (sc && (rc = fit(ws->post_b, 0))) return rc;
     }
     const size_t work_bytes = (size_t)(3 * (ws->cfg.max_iterations + 1) + 2) * 4;
     if (ws->work.bytes != work_bytes && (rc = ws->work.alloc(work_bytes))) return rc;
@@ -385,69 +431,36 @@ static int launch_words_to_rows(const unsigned* words, long long wpg, int B, int
     return MBP_OK;
 }
 
-template <class Real, int D, bool DAMP, bool ISO>
-static int launch_decode(mbp_workspace* ws, mbp::DecodeArgs<Real>& A, cudaStream_t s)
+template <class Real>
+static int dispatch_decode(mbp_workspace* ws, mbp::DecodeArgs<Real>& A, cudaStream_t s)
 {
-    auto kern = mbp::decode_kernel<Real, D, DAMP, ISO>;
-    int per_sm = 0;
-    MBP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, mbp::kDecodeThreads, 0));
-    if (per_sm < 1) return fail(MBP_ECUDA, "decode kernel cannot be resident");
-    const int grid = per_sm * ws->ens->sm_count;
-    void* args[] = {(void*)&A};
+    const bool damp = ws->cfg.damping != 0.0;
+    const bool iso = ws->cfg.combining_mode == MBP_ISOLATED_PER_MATRIX;
+    const int D = pick_degree(ws->ens->Ds);
     MBP_CUDA(cudaEventRecord(ws->ev0, s));
-    MBP_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(mbp::kDecodeThreads), args, 0, s));
+    cudaError_t err = sizeof(Real) == 8
+        ? mbp::launch_explicit_f64(reinterpret_cast<mbp::DecodeArgs<double>&>(A), D, damp, iso, ws->ens->sm_count, s)
+        : mbp::launch_explicit_f32(reinterpret_cast<mbp::DecodeArgs<float>&>(A), D, damp, iso, ws->ens->sm_count, s);
+    if (err == cudaErrorNotSupported) return fail(MBP_EUNSUPPORTED, "check degree too large");
+    MBP_CUDA(err);
     MBP_CUDA(cudaEventRecord(ws->ev1, s));
     ws->timed = true;
     return MBP_OK;
 }
 
-// Degree bound of the launch: the production variant (fp32, joint, no
-// damping) is instantiated for every exact max row degree up to 16 (no
-// padded compute), the others for powers of two.
-static int kernel_degree(int Ds, bool fast)
+static int dispatch_scatter(mbp_workspace* ws, const mbp::ScatterArgs& A, cudaStream_t s)
 {
-    if (fast) {
-        if (Ds <= 16) return std::max(Ds, 3);
-        for (int d : {20, 24, 28, 32, 48, 64}) if (Ds <= d) return d;
-        return 0;
-    }
-    return pick_degree(Ds);
-}
-
-template <class Real, int D>
-static int launch_variant(mbp_workspace* ws, mbp::DecodeArgs<Real>& A, cudaStream_t s)
-{
-    const bool damp = ws->cfg.damping != 0.0;
-    const bool iso = ws->cfg.combining_mode == MBP_ISOLATED_PER_MATRIX;
-    if (damp && iso) return launch_decode<Real, D, true, true>(ws, A, s);
-    if (damp) return launch_decode<Real, D, true, false>(ws, A, s);
-    if (iso) return launch_decode<Real, D, false, true>(ws, A, s);
-    return launch_decode<Real, D, false, false>(ws, A, s);
-}
-
-template <class Real>
-static int dispatch_decode(mbp_workspace* ws, mbp::DecodeArgs<Real>& A, cudaStream_t s)
-{
-    const bool fast = sizeof(Real) == 4 && ws->cfg.damping == 0.0 &&
-                      ws->cfg.combining_mode == MBP_JOINT_GRAPH;
-    const int D = kernel_degree(ws->ens->Ds, fast);
-    if (fast) {
-        switch (D) {
-#define MBP_FAST(DD) case DD: return launch_decode<float, DD, false, false>(ws, reinterpret_cast<mbp::DecodeArgs<float>&>(A), s);
-        MBP_FAST(3) MBP_FAST(4) MBP_FAST(5) MBP_FAST(6) MBP_FAST(7) MBP_FAST(8) MBP_FAST(9) MBP_FAST(10)
-        MBP_FAST(11) MBP_FAST(12) MBP_FAST(13) MBP_FAST(14) MBP_FAST(15) MBP_FAST(16) MBP_FAST(20)
-        MBP_FAST(24) MBP_FAST(28) MBP_FAST(32) MBP_FAST(48) MBP_FAST(64)
-#undef MBP_FAST
-        default: return fail(MBP_EUNSUPPORTED, "check degree too large");
-        }
-    }
-    switch (D) {
-    case 8: return launch_variant<Real, 8>(ws, A, s);
-    case 16: return launch_variant<Real, 16>(ws, A, s);
-    case 32: return launch_variant<Real, 32>(ws, A, s);
-    case 64: return launch_variant<Real, 64>(ws, A, s);
-    default: return fail(MBP_EUNSUPPORTED, "check degree too large");
-    }
+    const int D = scatter_degree(ws->ens->Ds);
+    const int sm = ws->ens->sm_count;
+    MBP_CUDA(cudaEventRecord(ws->ev0, s));
+    cudaError_t err = D <= 8 ? mbp::launch_scatter_small(A, D, sm, s)
+                    : D <= 16 ? mbp::launch_scatter_mid(A, D, sm, s)
+                              : mbp::launch_scatter_large(A, D, sm, s);
+    if (err == cudaErrorNotSupported) return fail(MBP_EUNSUPPORTED, "check degree too large");
+    MBP_CUDA(err);
+    MBP_CUDA(cudaEventRecord(ws->ev1, s));
+    ws->timed = true;
+    return MBP_OK;
 }
 
 template <class Real>
@@ -466,6 +479,104 @@ static __global__ void fill_post_prior_kernel(const unsigned* __restrict__ noisy
     }
 }
 
+// scatter-path state is kept in the noisy-relative domain (scatter.cuh):
+// post' = (-1)^y post.  Prior fill and readback convert.
+static __global__ void fill_rel_prior_kernel(const float* __restrict__ L, int G, int n, float* __restrict__ post)
+{
+    const long long total = (long long)G * n * 32;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < total;
+         k += (long long)gridDim.x * blockDim.x)
+        post[k] = L[(k >> 5) / n * 32 + (k & 31)];
+}
+
+static __global__ void gather_rel_post_kernel(const float* __restrict__ post_g, const unsigned* __restrict__ noisy_g,
+                                              int n, int lane, double* __restrict__ dst)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        const double v = post_g[(long long)i * 32 + lane];
+        dst[i] = ((noisy_g[i] >> lane) & 1u) ? -v : v;
+    }
+}
+
+// Scatter path (scatter.cuh) for one chunk of <= ws->cap frames.
+static int decode_chunk_scatter(mbp_workspace* ws, const uint8_t* noisy, const uint8_t* syn, const double* e,
+                                int e_stride, int B, uint8_t* corrected, uint8_t* conv, int* iters, int* mism,
+                                cudaStream_t s)
+{
+    const mbp_ensemble* ens = ws->ens;
+    const int G = (B + 31) / 32, F = G * 32;
+    const long long nb = (ens->n + 7) / 8, mb = (ens->m + 7) / 8;
+    const mbp_decoder_config& cfg = ws->cfg;
+    const int Dm = ens->Ds;
+    int rc;
+    // tables are laid out with the chunk's own frame stride F = 32 G
+    MBP_CUDA(cudaMemsetAsync(ws->sc_Lmax.p, 0, 4, s));
+    mbp::scatter_setup_kernel<<<(F + 127) / 128, 128, 0, s>>>(e, e_stride, B, F, Dm, (double)(float)cfg.llr_clamp,
+                                                               ws->Lmag.as<float>(), ws->sc_Mtab.as<float>(),
+                                                               ws->sc_Lmax.as<float>());
+    MBP_CUDA(cudaGetLastError());
+    if ((rc = launch_rows_to_words(noisy, nb, B, G, 1, ens->n, nb, ws->noisy_w.as<unsigned>(),
+                                   ws->hard_w.as<unsigned>(), ens->n, s)))
+        return rc;
+    if ((rc = launch_rows_to_words(syn, (long long)ens->u * mb, B, G, ens->u, ens->m, mb,
+                                   ws->syn_w.as<unsigned>(), nullptr, ens->C, s)))
+        return rc;
+    const bool record = (cfg.flags & MBP_RECORD_HISTORY) != 0;
+    if (record)
+        MBP_CUDA(cudaMemcpyAsync(ws->hist_w.p, ws->noisy_w.p, (size_t)G * ens->n * 4, cudaMemcpyDeviceToDevice, s));
+    if (cfg.flags & MBP_KEEP_STATE) {
+        // slot 0 holds the prior (+L in the noisy-relative domain) for frames
+        // that stop at iteration 0
+        fill_rel_prior_kernel<<<1024, 256, 0, s>>>(ws->Lmag.as<float>(), G, ens->n, ws->sc_post.as<float>());
+        MBP_CUDA(cudaGetLastError());
+    }
+    MBP_CUDA(cudaMemsetAsync(ws->cnt.p, 0, 2 * (size_t)F * 4, s));
+    MBP_CUDA(cudaMemsetAsync(ws->any_bad.p, 0, 8, s));
+    MBP_CUDA(cudaMemsetAsync(ws->iters.p, 0xff, (size_t)F * 4, s));
+    MBP_CUDA(cudaMemsetAsync(ws->barrier.p, 0, 8, s));
+    MBP_CUDA(cudaMemsetAsync(ws->work.p, 0, ws->work.bytes, s));
+    MBP_CUDA(cudaMemsetAsync(ws->sweeps.p, 0, 8, s));
+    if (ws->Gb) {
+        MBP_CUDA(cudaMemsetAsync(ws->ctrl.p, 0, ws->ctrl.bytes, s));
+        MBP_CUDA(cudaMemsetAsync(ws->fid_b.p, 0xff, ws->fid_b.bytes, s));
+        MBP_CUDA(cudaMemsetAsync(ws->src_b.p, 0xff, ws->src_b.bytes, s));
+        MBP_CUDA(cudaMemsetAsync(ws->newslot.p, 0xff, ws->newslot.bytes, s));
+    }
+    mbp::ScatterArgs A;
+    std::memset(&A, 0, sizeof A);
+    A.n = ens->n; A.m = ens->m; A.u = ens->u; A.C = ens->C; A.Ds = ens->Ds;
+    A.slots = (long long)ens->C * ens->Ds;
+    A.deg = ens->deg.as<uint8_t>(); A.chk_ell = ens->chk_ell.as<int>();
+    A.var_ptr = ens->var_ptr.as<int>(); A.var_chk = ens->var_chk.as<int>();
+    A.dv_max = ens->dmax_v; A.var_ptr_regular = ens->dv_reg == ens->dmax_v; A.Dm = Dm;
+    A.G = G; A.B = B;
+    A.post = ws->sc_post.as<float>(); A.acc = ws->sc_acc.as<int>(); A.c2v = ws->c2v.as<float>();
+    A.Lmag = ws->Lmag.as<float>(); A.Mtab = ws->sc_Mtab.as<float>();
+    A.Lfix = ws->sc_Lfix.as<int>(); A.Mfix = ws->sc_Mfix.as<int>();
+    A.noisy_w = ws->noisy_w.as<unsigned>(); A.syn_w = ws->syn_w.as<unsigned>(); A.mis_w = ws->sc_mis.as<unsigned>();
+    A.hard_w = ws->hard_w.as<unsigned>(); A.hist_w = record ? ws->hist_w.as<unsigned>() : nullptr;
+    A.cnt = ws->cnt.as<int>();
+    A.Gb = G >= 2 ? std::min(ws->Gb, (G + 1) / 2) : 0;
+    A.post_b = ws->sc_post_b.as<float>(); A.acc_b = ws->sc_acc_b.as<int>(); A.c2v_b = ws->c2v_b.as<float>();
+    A.Lmag_b = ws->Lmag_b.as<float>(); A.Mtab_b = ws->sc_Mtab_b.as<float>(); A.Lfix_b = ws->sc_Lfix_b.as<int>();
+    A.noisy_b = ws->noisy_b.as<unsigned>(); A.syn_b = ws->syn_b.as<unsigned>(); A.mis_b = ws->sc_mis_b.as<unsigned>();
+    A.hard_b = ws->hard_b.as<unsigned>(); A.cnt_b = ws->cnt_b.as<int>(); A.fid_b = ws->fid_b.as<int>();
+    A.src_b = ws->src_b.as<int>(); A.newslot = ws->newslot.as<int>(); A.grp_cnt = ws->grp_cnt.as<int>();
+    A.ctrl = ws->ctrl.as<int>();
+    A.any_bad = ws->any_bad.as<int>(); A.iters = ws->iters.as<int>();
+    A.barrier = ws->barrier.as<unsigned>(); A.work = ws->work.as<unsigned>(); A.sweeps_run = ws->sweeps.as<int>();
+    A.ts = ws->ts_cap ? ws->ts.as<unsigned long long>() : nullptr; A.ts_cap = ws->ts_cap;
+    A.Lmax = ws->sc_Lmax.as<float>();
+    A.out_conv = conv; A.out_iters = iters; A.out_mism = mism;
+    A.max_it = cfg.max_iterations; A.clamp = (float)cfg.llr_clamp; A.sat = ens->sat;
+    if ((rc = dispatch_scatter(ws, A, s))) return rc;
+    if ((rc = launch_words_to_rows(ws->hard_w.as<unsigned>(), ens->n, B, G, 1, ens->n, nb, corrected, nb, s)))
+        return rc;
+    ws->last_B = B;
+    return MBP_OK;
+}
+
 template <class Real>
 static int decode_chunk(mbp_workspace* ws, const uint8_t* noisy, const uint8_t* syn, const double* e,
                         int e_stride, int B, uint8_t* corrected, uint8_t* conv, int* iters, int* mism,
@@ -476,6 +587,8 @@ static int decode_chunk(mbp_workspace* ws, const uint8_t* noisy, const uint8_t* 
     const long long nb = (ens->n + 7) / 8, mb = (ens->m + 7) / 8;
     const mbp_decoder_config& cfg = ws->cfg;
     int rc;
+    if (sizeof(Real) == 4 && ws->scatter)
+        return decode_chunk_scatter(ws, noisy, syn, e, e_stride, B, corrected, conv, iters, mism, s);
     mbp::prior_kernel<Real><<<(F + 255) / 256, 256, 0, s>>>(e, e_stride, B, F, ws->Lmag.as<Real>());
     MBP_CUDA(cudaGetLastError());
     if ((rc = launch_rows_to_words(noisy, nb, B, G, 1, ens->n, nb, ws->noisy_w.as<unsigned>(),
@@ -684,8 +797,25 @@ int mbp_workspace_read_posterior(mbp_workspace* ws, int64_t frame, double* poste
     DeviceGuard dg(ens->device);
     MBP_CUDA(cudaStreamSynchronize(ws->own_stream));
     MBP_CUDA(cudaDeviceSynchronize());
-    const size_t P = ws->cfg.combining_mode == MBP_ISOLATED_PER_MATRIX ? (size_t)ens->u + 1 : 1;
     const size_t g = frame / 32;
+    if (ws->scatter) {
+        // post_t lives in slot t & 1; a frame's last sweep is its converged
+        // iteration (0: the prior, kept in slot 0) or max_iterations
+        int it = -1;
+        MBP_CUDA(cudaMemcpy(&it, ws->iters.as<int>() + frame, 4, cudaMemcpyDeviceToHost));
+        const int last = it >= 0 ? it : ws->cfg.max_iterations;
+        const size_t Gc = (ws->last_B + 31) / 32;
+        const float* base = ws->sc_post.as<float>() + ((size_t)(last & 1) * Gc + g) * ens->n * 32;
+        DevBuf tmp;
+        int rc;
+        if ((rc = tmp.alloc((size_t)ens->n * 8))) return rc;
+        gather_rel_post_kernel<<<(ens->n + 255) / 256, 256>>>(base, ws->noisy_w.as<unsigned>() + g * ens->n, ens->n,
+                                                              (int)(frame & 31), tmp.as<double>());
+        MBP_CUDA(cudaGetLastError());
+        MBP_CUDA(cudaMemcpy(posterior, tmp.p, (size_t)ens->n * 8, cudaMemcpyDeviceToHost));
+        return MBP_OK;
+    }
+    const size_t P = ws->cfg.combining_mode == MBP_ISOLATED_PER_MATRIX ? (size_t)ens->u + 1 : 1;
     const char* base = ws->post.as<char>() + ((g * P + (P - 1)) * ens->n * 32) * ws->real_size;
     return read_lane(ws, base, ens->n, frame, posterior);
 }
@@ -694,6 +824,8 @@ int mbp_workspace_read_c2v(mbp_workspace* ws, int64_t frame, double* c2v)
 {
     if (!ws || !c2v) return fail(MBP_EINVAL, "null pointer argument");
     if (!(ws->cfg.flags & MBP_KEEP_STATE)) return fail(MBP_EINVAL, "workspace was not configured with MBP_KEEP_STATE");
+    if (ws->scatter)
+        return fail(MBP_EINVAL, "the scatter decode path does not keep messages; configure MBP_EXPLICIT_MESSAGES");
     if (frame < 0 || frame >= ws->last_B) return fail(MBP_EINVAL, "frame outside the last batch");
     const mbp_ensemble* ens = ws->ens;
     DeviceGuard dg(ens->device);

@@ -1,0 +1,821 @@
+// scatter.cuh -- the production decode kernel: fp32, joint graph, no damping.
+//
+// Same flooding schedule, stopping rule and outputs as decode_kernel
+// (decode.cuh; decode_loop, _kernels.py:323-379), restructured so that the
+// edge messages of the common 2-3 sweep decode never touch HBM:
+//
+//  * sweep 1 needs no check phase.  Its inputs are the unclamped priors +-L
+//    (_kernels.py:353-355), so every message of check j is
+//        c2v_1(j -> b) = (-1)^(s_j xor y_b) * M_{d_j}(L),
+//    s_j = the iteration-0 mismatch bit of check j (z_j xor parity of the
+//    noisy key over the row), M_d(L) = 2 atanh(tanh(L/2)^(d-1)) clamped --
+//    the reference's product of d-1 equal factors (c2v_pass,
+//    _kernels.py:240-258), evaluated once per frame and degree in fp64.
+//    The sweep-1 posterior is a gather of bits and table entries.
+//  * posteriors are accumulated from the check side: a check phase adds its
+//    new messages into acc[var] with red.global.add.s32 on fixed-point
+//    values round(c2v * 2^S) (S chosen per launch so |acc| < 2^30).  Integer
+//    addition is associative, so the posterior is deterministic and
+//    independent of the order the checks run in; its error (<= dv * 2^-S-1)
+//    is of the order of the fp32 summation it replaces.  The variable phase
+//    only converts acc -> post (fp32), takes the hard decision (acc < 0,
+//    ties -> 0 as in hard_pass, _kernels.py:304-307) and re-arms acc with the
+//    prior.
+//  * c2v_{t-1}, needed as the extrinsic correction v2c = post - c2v
+//    (_kernels.py:276-281), is recomputed rather than stored for t <= 3:
+//    sweep 2 rebuilds c2v_1 from bits, sweep 3 rebuilds c2v_1 and c2v_2 from
+//    the stored sweep-1 posterior.  From sweep kStoreFrom on, c2v_t is also
+//    stored (the few frames that need 4+ sweeps read it back).
+//  * everything runs in the noisy-relative domain: for variable b the kernel
+//    keeps post'_b = (-1)^y_b post_b and c2v'(j -> b) = (-1)^y_b c2v(j -> b)
+//    (y = noisy key bit).  Negation is exact and commutes with clamp and
+//    round-to-nearest, so this is the reference's arithmetic bit for bit, up
+//    to the sign.  In this domain the prior is +L for every bit, Eq. 6's
+//    syndrome sign (-1)^z_j becomes (-1)^s_j (z_j xor the row's noisy
+//    parity), and every sweep-1 message of check j is the same value
+//    (-1)^s_j M_{d_j}: the check phase needs no per-edge key bits.  The hard
+//    decision is post_b < 0  <=>  (y_b ? post'_b > 0 : post'_b < 0).
+//  * Eq. 6 in (S, Delta) form: with u = e^-|x|, tanh(|x|/2) = (1-u)/(1+u);
+//    for a set of edges A = prod(1+u), B = prod(1-u), S = A + B, D = A - B
+//    combine as (S, D) x (1, u) = (S + uD, D + uS) -- only additions of
+//    non-negative terms, so no cancellation where the product of tanh values
+//    approaches 1 (the naive fp32 failure) -- and the
+//    message is 2 atanh(B/A) = ln(S/D).  Exclusive products come from prefix
+//    and suffix pairs; 3 MUFU per edge (ex2, 2 x lg2).
+//
+// Layout as in kernels.cuh (lane = frame, groups of 32 frames), plus
+//   post[2][Gc][n][32] f32    post_s lives in slot s & 1
+//   acc[Gc][n][32]     s32    fixed-point posterior being accumulated
+//   mis_w[Gc][C]       u32    iteration-0 mismatch words
+//   Mtab[Dm+1][Fc]     f32    sweep-1 message magnitude per degree and frame
+// (Gc = groups of the layout's allocation, Fc = 32 Gc).
+#pragma once
+
+#include "decode.cuh"
+
+namespace mbp {
+
+constexpr int kStoreFrom = 3;   // c2v_t is stored for t >= kStoreFrom
+
+#ifndef MBP_SCATTER_MIN_BLOCKS
+#define MBP_SCATTER_MIN_BLOCKS 4
+#endif
+
+struct ScatterArgs {
+    // graph
+    int n, m, u, C, Ds;
+    long long slots;                  // C * Ds
+    const uint8_t* __restrict__ deg;  // [C]
+    const int* __restrict__ chk_ell;  // [C*Ds]
+    const int* __restrict__ var_ptr;  // [n+1] CSR into var_chk
+    const int* __restrict__ var_chk;  // stacked check id of each edge, ascending edge order per variable
+    int dv_max;
+    int var_ptr_regular;              // every variable has degree dv_max (var_chk is [n][dv_max])
+    int Dm;                           // Mtab degree bound (= Ds)
+    // primary layout
+    int G, B;
+    float* post;
+    int* acc;
+    float* c2v;
+    const float* Lmag;                // [F]
+    const float* Mtab;                // [Dm+1][F]
+    int* Lfix;                        // [F]   round(L * 2^S), written by the kernel
+    int* Mfix;                        // [Dm+1][F]
+    const unsigned* noisy_w;
+    const unsigned* syn_w;
+    unsigned* mis_w;
+    unsigned* hard_w;
+    unsigned* hist_w;
+    int* cnt;
+    // compacted layout (capacity Gb groups)
+    int Gb;
+    float* post_b;
+    int* acc_b;
+    float* c2v_b;
+    float* Lmag_b;
+    float* Mtab_b;
+    int* Lfix_b;
+    unsigned* noisy_b;
+    unsigned* syn_b;
+    unsigned* mis_b;
+    unsigned* hard_b;
+    int* cnt_b;
+    int* fid_b;
+    int* src_b;
+    int* newslot;
+    int* grp_cnt;
+    int* ctrl;
+    // control
+    int* any_bad;
+    int* iters;
+    unsigned* barrier;
+    unsigned* work;
+    int* sweeps_run;
+    unsigned long long* ts;
+    int ts_cap;
+    const float* Lmax;                // [1] max prior magnitude of the batch
+    // outputs
+    uint8_t* out_conv;
+    int* out_iters;
+    int* out_mism;
+    // config
+    int max_it;
+    float clamp;
+    float sat;
+};
+
+template <bool CPT>
+struct SL {
+    const ScatterArgs& A;
+    int G;                            // groups of the current layout
+    __device__ __forceinline__ int Gc() const { return CPT ? A.Gb : A.G; }
+    __device__ __forceinline__ float* post(int sweep) const
+    {
+        return (CPT ? A.post_b : A.post) + (size_t)(sweep & 1) * Gc() * A.n * 32;
+    }
+    __device__ __forceinline__ int* acc() const { return CPT ? A.acc_b : A.acc; }
+    __device__ __forceinline__ float* c2v() const { return CPT ? A.c2v_b : A.c2v; }
+    __device__ __forceinline__ unsigned* hard_w() const { return CPT ? A.hard_b : A.hard_w; }
+    __device__ __forceinline__ unsigned* mis() const { return CPT ? A.mis_b : A.mis_w; }
+    __device__ __forceinline__ int* cnt() const { return CPT ? A.cnt_b : A.cnt; }
+    __device__ __forceinline__ unsigned noisy(size_t w) const { return CPT ? ld_cg(A.noisy_b + w) : ld_ro(A.noisy_w + w); }
+    __device__ __forceinline__ unsigned syn(size_t w) const { return CPT ? ld_cg(A.syn_b + w) : ld_ro(A.syn_w + w); }
+    __device__ __forceinline__ float M1(int d, int s) const
+    {
+        return CPT ? ld_cg(A.Mtab_b + (size_t)d * Gc() * 32 + s) : ld_ro(A.Mtab + (size_t)d * Gc() * 32 + s);
+    }
+    __device__ __forceinline__ int Lfix(int s) const { return ld_cg((CPT ? A.Lfix_b : A.Lfix) + s); }
+};
+
+// ptxas branches around a lane-predicated REDG (BSSY/BRA/BSYNC per edge), so
+// dead lanes add 0 instead: the warp's line request is issued either way.
+__device__ __forceinline__ void red_add(int* p, int v)
+{
+    asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Eq. 6, (S, Delta) form (header comment).  Slots k >= d (PAD) and inputs
+// with |x| >= sat (where the reference's float64 tanh(x/2) is exactly 1.0)
+// get u = 0, the neutral factor (1, 0); a message whose other factors are
+// all neutral has D = 0 -> ln(S/0) = inf -> +-clamp, the reference's
+// `prod >= 1.0` branch (_kernels.py:249-252).
+// ---------------------------------------------------------------------------
+template <int DD, bool PAD>
+__device__ __forceinline__ void rule_sd(const float (&x)[DD], int d, unsigned flip, float clamp, float sat,
+                                        float (&out)[DD])
+{
+    float uu[DD];
+    unsigned sb[DD];
+    unsigned tot = flip << 31;
+#pragma unroll
+    for (int k = 0; k < DD; ++k) {
+        const bool in = !PAD || k < d;
+        const float a = fabsf(x[k]);
+        const float u = ex2_approx(-1.44269504088896341f * a);
+        uu[k] = (in && a < sat) ? u : 0.0f;
+        sb[k] = in ? (__float_as_uint(x[k]) & 0x80000000u) : 0u;
+        tot ^= sb[k];
+    }
+    float sS[DD], sD[DD];
+    float S = 1.0f, Dl = 0.0f;
+#pragma unroll
+    for (int k = DD - 1; k >= 0; --k) {
+        sS[k] = S;
+        sD[k] = Dl;
+        const float S2 = fmaf(Dl, uu[k], S);
+        Dl = fmaf(S, uu[k], Dl);
+        S = S2;
+    }
+    float pS = 1.0f, pD = 0.0f;
+#pragma unroll
+    for (int k = 0; k < DD; ++k) {
+        const float eS = fmaf(pS, sS[k], pD * sD[k]);
+        const float eD = fmaf(pS, sD[k], pD * sS[k]);
+        const float mag = fminf((lg2_approx(eS) - lg2_approx(eD)) * 0.69314718055994531f, clamp);
+        out[k] = __uint_as_float(__float_as_uint(mag) | (tot ^ sb[k]));
+        const float S2 = fmaf(pD, uu[k], pS);
+        pD = fmaf(pS, uu[k], pD);
+        pS = S2;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// check phase: check j of group g at sweep t >= 2.  srow = the row's variable
+// ids (staged), d its degree (<= DD), mis/syn words of the row, M1 = this
+// lane's sweep-1 magnitude for degree d, qrow = c2v_{t-1} row base (explicit
+// base only).  Computes c2v_t, adds it into acc, stores it for t >= kStoreFrom.
+// ---------------------------------------------------------------------------
+template <int DD, bool PAD, bool CPT>
+__device__ __forceinline__ void sc_check_item(const ScatterArgs& A, const SL<CPT>& S, int g, int j, int t,
+                                              bool live, int lane, const int* srow, int d, unsigned misword,
+                                              float M1, const float* qrow, float scale)
+{
+    const unsigned sj = (misword >> lane) & 1u;        // relative-domain syndrome sign
+    const size_t gl = (size_t)g * A.n * 32 + lane;     // element (g, 0, lane)
+    unsigned off[DD];
+#pragma unroll
+    for (int k = 0; k < DD; ++k) off[k] = (!PAD || k < d) ? (unsigned)srow[k] * 32u : 0u;
+    const bool explicit_base = t > kStoreFrom;
+    float c[DD];
+    if (!explicit_base) {
+        const float c1 = sj ? -M1 : M1;                 // c2v'_1, the same on every edge
+#pragma unroll
+        for (int k = 0; k < DD; ++k) c[k] = c1;
+    } else {
+#pragma unroll
+        for (int k = 0; k < DD; ++k) c[k] = ld_cg_if(qrow + k * 32, live && (!PAD || k < d));
+    }
+    // c2v'_s from c2v'_{s-1} and post'_{s-1}, s = first..t
+    for (int s = explicit_base ? t : 2; s <= t; ++s) {
+        const float* pp = S.post(s - 1) + gl;
+        float x[DD];
+#pragma unroll
+        for (int k = 0; k < DD; ++k) {
+            const float p = ld_cg_if(pp + off[k], live && (!PAD || k < d));
+            x[k] = clampr(p - c[k], A.clamp);
+        }
+        rule_sd<DD, PAD>(x, d, sj, A.clamp, A.sat, c);
+    }
+    int* accg = S.acc() + gl;
+#pragma unroll
+    for (int k = 0; k < DD; ++k) {
+        const int v = __float2int_rn(c[k] * scale);
+        red_add(accg + off[k], (live && (!PAD || k < d)) ? v : 0);   // pads: off = 0
+    }
+    if (t >= kStoreFrom) {
+        float* crow = S.c2v() + ((size_t)g * A.slots + (size_t)j * A.Ds) * 32 + lane;
+#pragma unroll
+        for (int k = 0; k < DD; ++k) st_if(crow + k * 32, c[k], live && (!PAD || k < d));
+    }
+}
+
+template <int D, bool CPT>
+__device__ __forceinline__ void sc_check_dispatch(const ScatterArgs& A, const SL<CPT>& S, int g, int j, int t,
+                                                  bool live, int lane, const int* srow, int d, unsigned misword,
+                                                  float M1, const float* qrow, float scale)
+{
+    // the row degree is warp-uniform: exact-degree code for the two most
+    // common degrees (D and D-1), padded code for the rest
+    if (d == D)
+        sc_check_item<D, false, CPT>(A, S, g, j, t, live, lane, srow, d, misword, M1, qrow, scale);
+    else if (D > 1 && d == D - 1)
+        sc_check_item<(D > 1 ? D - 1 : 1), false, CPT>(A, S, g, j, t, live, lane, srow, d, misword, M1, qrow, scale);
+    else
+        sc_check_item<D, true, CPT>(A, S, g, j, t, live, lane, srow, d, misword, M1, qrow, scale);
+}
+
+// c2v_{t-1} row base for lane `lane` of group g (explicit base only); the
+// first sweep after a compaction reads it in place from the frame's
+// original lane of the primary layout.
+template <bool CPT>
+__device__ __forceinline__ const float* sc_c2v_in_base(const ScatterArgs& A, const SL<CPT>& S, int g, int lane,
+                                                       bool first_after_compaction)
+{
+    if (CPT && first_after_compaction) {
+        const int s = ld_cg(A.src_b + g * 32 + lane);
+        if (s >= 0) return A.c2v + (size_t)(s >> 5) * A.slots * 32 + (s & 31);
+    }
+    return S.c2v() + (size_t)g * A.slots * 32 + lane;
+}
+
+template <int D, bool CPT>
+__device__ __forceinline__ void sc_check_chunk(const ScatterArgs& A, const SL<CPT>& S, int base, int end, int t,
+                                               const int* cprev, int lane, int* s_idx, unsigned* s_w,
+                                               unsigned* s_m, int* s_d, bool first, float scale)
+{
+    constexpr int SD = Chunk<D>::SD;
+    const int rows = end - base;
+    if (lane < rows) {
+        const int item = base + lane;
+        const int j = item % A.C;
+        const int d = ld_ro(A.deg + j);
+        s_d[lane] = d;
+        s_m[lane] = ld_cg(S.mis() + item);     // mis index == item (g*C + j)
+        const int* row = A.chk_ell + (size_t)j * A.Ds;
+#pragma unroll
+        for (int k = 0; k < D; ++k)
+            if (k < d) s_idx[lane * SD + k] = ld_ro(row + k);
+    }
+    __syncwarp();
+    int g = base / A.C;
+    int j = base - g * A.C;
+    unsigned act = group_mask(cprev, g, lane);
+    const float* qb = t > kStoreFrom ? sc_c2v_in_base<CPT>(A, S, g, lane, first) : nullptr;
+    for (int r = 0; r < rows; ++r) {
+        if (act) {
+            const int d = s_d[r];
+            const float M1 = t <= kStoreFrom ? S.M1(d, g * 32 + lane) : 0.0f;
+            const float* qrow = qb ? qb + (size_t)j * A.Ds * 32 : nullptr;
+            sc_check_dispatch<D, CPT>(A, S, g, j, t, (act >> lane) & 1u, lane, s_idx + r * SD, d, s_m[r], M1,
+                                      qrow, scale);
+        }
+        if (++j == A.C && r + 1 < rows) {
+            j = 0;
+            ++g;
+            act = group_mask(cprev, g, lane);
+            qb = t > kStoreFrom ? sc_c2v_in_base<CPT>(A, S, g, lane, first) : nullptr;
+        }
+    }
+    __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// variable phases
+// ---------------------------------------------------------------------------
+
+// sweep 1: post_1 = prior + sum of the sweep-1 messages, in fixed point
+// (exactly what the check-side accumulation of later sweeps computes).
+// Lanes load the variable's check ids, mismatch words and degrees, then the
+// warp walks them with shuffles.  Also arms acc with the prior for sweep 2.
+template <bool CPT>
+__device__ __forceinline__ void sc_var1_item(const ScatterArgs& A, const SL<CPT>& S, int g, int i, unsigned act,
+                                             int lane, const int* Mfix, int Lf, float iscale)
+{
+    const bool live = (act >> lane) & 1u;
+    const size_t w = (size_t)g * A.n + i;
+    const unsigned yw = S.noisy(w);
+    const unsigned y = (yw >> lane) & 1u;
+    int a = Lf;
+    const int p0 = ld_ro(A.var_ptr + i), dv = ld_ro(A.var_ptr + i + 1) - p0;
+    for (int base = 0; base < dv; base += 32) {
+        unsigned mk = 0;
+        int dk = 0;
+        if (base + lane < dv) {
+            const int j = ld_ro(A.var_chk + p0 + base + lane);
+            mk = ld_cg(S.mis() + (size_t)g * A.C + j);
+            dk = ld_ro(A.deg + j);
+        }
+        const int cntk = min(32, dv - base);
+        for (int k = 0; k < cntk; ++k) {
+            const unsigned mw = __shfl_sync(kFull, mk, k);
+            const int d = __shfl_sync(kFull, dk, k);
+            const int mf = ld_cg(Mfix + (size_t)d * S.Gc() * 32);
+            a += ((mw >> lane) & 1u) ? -mf : mf;
+        }
+    }
+    st_if(S.post(1) + w * 32 + lane, (float)a * iscale, live);
+    if (live) S.acc()[w * 32 + lane] = Lf;
+    const unsigned neg = __ballot_sync(kFull, y ? a > 0 : a < 0);
+    if (lane == 0) {
+        // the iteration-0 decision of every frame is its noisy key
+        const unsigned hw = (neg & act) | (yw & ~act);
+        S.hard_w()[w] = hw;
+        if (A.hist_w) A.hist_w[((size_t)1 * A.G) * A.n + w] = hw;
+    }
+}
+
+// Sweep 1 for a regular column degree DV <= 16: one chunk of <= 32
+// variables.  The chunk's check ids, mismatch words and degrees are staged
+// in shared memory with independent loads (two dependent round trips per
+// chunk), the lane's Mfix row per degree sits in a shared table.
+template <int D, int DV, bool CPT>
+__device__ __forceinline__ void sc_var1_chunk(const ScatterArgs& A, const SL<CPT>& S, int base, int end,
+                                              const int* cprev, int lane, unsigned* s_mis, uint8_t* s_deg,
+                                              int* s_mf, float iscale)
+{
+    const int rows = end - base;
+    const int tot = rows * DV;
+#pragma unroll 4
+    for (int idx = lane; idx < tot; idx += 32) {
+        const int v = idx / DV, k = idx - v * DV;
+        const int item = base + v;
+        const int g = item / A.n, i = item - g * A.n;
+        const int j = ld_ro(A.var_chk + (size_t)i * DV + k);
+        s_mis[idx] = ld_cg(S.mis() + (size_t)g * A.C + j);
+        s_deg[idx] = ld_ro(A.deg + j);
+    }
+    __syncwarp();
+    int r = 0;
+    while (r < rows) {
+        const int item = base + r;
+        const int g = item / A.n;
+        const int i = item - g * A.n;
+        const int span = min(rows - r, A.n - i);
+        const unsigned act = group_mask(cprev, g, lane);
+        if (act) {
+#pragma unroll
+            for (int d = 0; d <= D; ++d) s_mf[d * 32 + lane] = ld_cg(A.Mfix + (size_t)d * A.G * 32 + g * 32 + lane);
+            __syncwarp();
+            const bool live = (act >> lane) & 1u;
+            const int Lf = S.Lfix(g * 32 + lane);
+            for (int v = r; v < r + span; ++v) {
+                const size_t w = (size_t)base + v;
+                const unsigned yw = S.noisy(w);
+                const unsigned y = (yw >> lane) & 1u;
+                int a = Lf;
+#pragma unroll
+                for (int k = 0; k < DV; ++k) {
+                    const unsigned mw = s_mis[v * DV + k];
+                    const int mf = s_mf[s_deg[v * DV + k] * 32 + lane];
+                    a += ((mw >> lane) & 1u) ? -mf : mf;
+                }
+                st_if(S.post(1) + w * 32 + lane, (float)a * iscale, live);
+                if (live) S.acc()[w * 32 + lane] = Lf;
+                const unsigned neg = __ballot_sync(kFull, y ? a > 0 : a < 0);
+                if (lane == 0) {
+                    // the iteration-0 decision of every frame is its noisy key
+                    const unsigned hw = (neg & act) | (yw & ~act);
+                    S.hard_w()[w] = hw;
+                    if (A.hist_w) A.hist_w[((size_t)1 * A.G) * A.n + w] = hw;
+                }
+            }
+            __syncwarp();
+        }
+        r += span;
+    }
+    __syncwarp();
+}
+
+// sweep t >= 2: acc -> post_t, hard decision, re-arm acc with the prior.
+template <bool CPT>
+__device__ __forceinline__ void sc_var_chunk(const ScatterArgs& A, const SL<CPT>& S, int base, int end, int t,
+                                             const int* cprev, int lane, unsigned* s_w, unsigned* s_old,
+                                             float iscale)
+{
+    const int rows = end - base;
+    if (lane < rows) {
+        s_w[lane] = S.noisy(base + lane);
+        s_old[lane] = ld_cg(S.hard_w() + base + lane);
+    }
+    __syncwarp();
+    float* postt = S.post(t);
+    int* acc = S.acc();
+    int r = 0;
+    while (r < rows) {
+        const int item = base + r;
+        const int g = item / A.n;
+        const int i = item - g * A.n;
+        const int span = min(rows - r, A.n - i);
+        const unsigned act = group_mask(cprev, g, lane);
+        if (act) {
+            const bool live = (act >> lane) & 1u;
+            const int Lf = S.Lfix(g * 32 + lane);
+            constexpr int U = 4;   // independent acc loads in flight
+            for (int k0 = 0; k0 < span; k0 += U) {
+                int a[U];
+#pragma unroll
+                for (int v = 0; v < U; ++v) {
+                    const size_t w = (size_t)item + k0 + v;
+                    a[v] = (k0 + v < span && live) ? ld_cg(acc + w * 32 + lane) : 0;
+                }
+#pragma unroll
+                for (int v = 0; v < U; ++v) {
+                    if (k0 + v >= span) break;
+                    const size_t w = (size_t)item + k0 + v;
+                    const unsigned y = (s_w[r + k0 + v] >> lane) & 1u;
+                    st_if(postt + w * 32 + lane, (float)a[v] * iscale, live);
+                    if (live) acc[w * 32 + lane] = Lf;
+                    const unsigned neg = __ballot_sync(kFull, y ? a[v] > 0 : a[v] < 0);
+                    if (lane == 0) {
+                        const unsigned hw = (neg & act) | (s_old[r + k0 + v] & ~act);
+                        S.hard_w()[w] = hw;
+                        if (A.hist_w) A.hist_w[((size_t)t * A.G) * A.n + w] = hw;
+                    }
+                }
+            }
+        }
+        r += span;
+    }
+    __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// syndrome phase (as syncheck_item); at t = 0 also stores the mismatch words
+// ---------------------------------------------------------------------------
+template <bool CPT>
+__device__ __forceinline__ void sc_syncheck_item(const ScatterArgs& A, const SL<CPT>& S, int g, int blk, int t,
+                                                 unsigned act, int lane)
+{
+    const int j = blk * 32 + lane;
+    unsigned mism = 0;
+    if (j < A.C) {
+        const unsigned* hw = S.hard_w() + (size_t)g * A.n;
+        const int d = ld_ro(A.deg + j);
+        const int* row = A.chk_ell + (size_t)j * A.Ds;
+        unsigned par = 0;
+        for (int k = 0; k < d; ++k) par ^= ld_cg(hw + ld_ro(row + k));
+        const unsigned full = par ^ S.syn((size_t)g * A.C + j);
+        if (t == 0) S.mis()[(size_t)g * A.C + j] = full;
+        mism = full & act;
+    }
+    int c = 0;
+#pragma unroll
+    for (int f = 0; f < 32; ++f) {
+        const int pc = __popc(__ballot_sync(kFull, (mism >> f) & 1u));
+        if (lane == f) c = pc;
+    }
+    if (c) atomicAdd(S.cnt() + (t & 1) * S.G * 32 + g * 32 + lane, c);
+    if (__any_sync(kFull, c != 0) && lane == 0) atomicOr(A.any_bad + (t & 1), 1);
+}
+
+// ---------------------------------------------------------------------------
+// compaction (cf. decode.cuh compact()): repack the undecided frames into
+// dense groups of the secondary layout at the start of sweep t >= 2
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int sc_compact(const ScatterArgs& A, int t, int gw, int nw, int gtid, int nthreads,
+                                          int lane)
+{
+    const int F = A.G * 32;
+    const int* cprev = A.cnt + ((t - 1) & 1) * F;
+    stamp_compact(A, 0);
+    if (blockIdx.x == 0) {
+        __shared__ int s_part[kDecodeThreads];
+        const int per = (A.G + blockDim.x - 1) / blockDim.x;
+        const int g0 = threadIdx.x * per, g1 = min(A.G, g0 + per);
+        int sum = 0;
+        for (int g = g0; g < g1; ++g) sum += ld_cg(A.grp_cnt + g);
+        s_part[threadIdx.x] = sum;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int run = 0;
+            for (int k = 0; k < (int)blockDim.x; ++k) { const int v = s_part[k]; s_part[k] = run; run += v; }
+        }
+        __syncthreads();
+        int run = s_part[threadIdx.x];
+        for (int g = g0; g < g1; ++g) { const int v = ld_cg(A.grp_cnt + g); A.grp_cnt[g] = run; run += v; }
+    }
+    grid_barrier(A.barrier);
+    for (int g = gw; g < A.G; g += nw) {
+        const bool und = ld_cg(cprev + g * 32 + lane) != 0;
+        const unsigned msk = __ballot_sync(kFull, und);
+        if (und) {
+            const int s2 = ld_cg(A.grp_cnt + g) + __popc(msk & ((1u << lane) - 1u));
+            A.newslot[g * 32 + lane] = s2;
+            A.src_b[s2] = g * 32 + lane;
+            A.fid_b[s2] = g * 32 + lane;
+        }
+    }
+    grid_barrier(A.barrier);
+    stamp_compact(A, 1);
+    const int nund = ld_cg(A.ctrl + 2 * t);
+    const int Gn = (nund + 31) / 32;
+    const int Fb = Gn * 32;
+    const size_t slotP = (size_t)A.G * A.n * 32, slotB = (size_t)A.Gb * A.n * 32;
+    // posteriors the next check phase reads: post_1..post_{t-1} while the
+    // base is rebuilt from bits (t <= kStoreFrom), else post_{t-1}
+    for (int s = (t <= kStoreFrom ? 1 : t - 1); s <= t - 1; ++s)
+        move_lanes<float>(A.post + (s & 1) * slotP, A.post_b + (s & 1) * slotB, A.n, Gn, A.src_b, gw, nw, lane);
+    move_bits(A.noisy_w, A.noisy_b, A.n, Gn, A.src_b, gw, nw, lane);
+    move_bits(A.hard_w, A.hard_b, A.n, Gn, A.src_b, gw, nw, lane);
+    move_bits(A.syn_w, A.syn_b, A.C, Gn, A.src_b, gw, nw, lane);
+    move_bits(A.mis_w, A.mis_b, A.C, Gn, A.src_b, gw, nw, lane);
+    // acc armed with the prior (+L in the relative domain)
+    {
+        const long long total = (long long)Gn * A.n;
+        for (long long it = gw; it < total; it += nw) {
+            const int g2 = (int)(it / A.n), i = (int)(it - (long long)g2 * A.n);
+            const int s = ld_cg(A.src_b + g2 * 32 + lane);
+            A.acc_b[((size_t)g2 * A.n + i) * 32 + lane] = s >= 0 ? ld_cg(A.Lfix + s) : 0;
+        }
+    }
+    for (int s2 = gtid; s2 < Fb; s2 += nthreads) {
+        const int s = ld_cg(A.src_b + s2);
+        A.Lmag_b[s2] = s >= 0 ? A.Lmag[s] : 0.0f;
+        A.Lfix_b[s2] = s >= 0 ? ld_cg(A.Lfix + s) : 0;
+        for (int d = 0; d <= A.Dm; ++d)
+            A.Mtab_b[(size_t)d * A.Gb * 32 + s2] = s >= 0 ? A.Mtab[(size_t)d * A.G * 32 + s] : 0.0f;
+        A.cnt_b[((t - 1) & 1) * Fb + s2] = s >= 0 ? ld_cg(cprev + s) : 0;
+        A.cnt_b[(t & 1) * Fb + s2] = 0;
+    }
+    stamp_compact(A, 2);
+    grid_barrier(A.barrier);
+    stamp_compact(A, 3);
+    if (gtid == 0) A.sweeps_run[1] = t;
+    return Gn;
+}
+
+// ---------------------------------------------------------------------------
+// one sweep t in a given layout
+// ---------------------------------------------------------------------------
+template <int D, bool CPT>
+__device__ __forceinline__ void sc_sweep(const ScatterArgs& A, int G, int t, int& wc, int& ts_k, int lane, int nwarps,
+                                         int* s_idx, unsigned* s_w, unsigned* s_x, unsigned* s_m, unsigned* s_v1m,
+                                         uint8_t* s_v1d, int* s_mf, bool first, float scale, float iscale)
+{
+    const SL<CPT> S{A, G};
+    constexpr int CH = Chunk<D>::CH;
+    const int cblk = (A.C + 31) / 32;
+    const int* cp = S.cnt() + ((t - 1) & 1) * G * 32;
+    if (t >= 2) {   // check phase
+        const int total = G * A.C;
+        const int ch = chunk_size(total, nwarps, CH);
+        for (int base = claim(A.work + wc, lane, ch); base < total; base = claim(A.work + wc, lane, ch))
+            sc_check_chunk<D, CPT>(A, S, base, min(base + ch, total), t, cp, lane, s_idx, s_w, s_m,
+                                   reinterpret_cast<int*>(s_x), first, scale);
+        ++wc;
+        grid_barrier(A.barrier);
+        stamp(A, ts_k);
+    } else {
+        stamp(A, ts_k);   // keep three stamps per sweep
+    }
+    {   // variable phase
+        const int total = G * A.n;
+        const bool v1_staged = D <= 16 && (A.dv_max == 6 || A.dv_max == 9) && A.var_ptr_regular;
+        if (t == 1 && v1_staged) {
+            if constexpr (D <= 16) {
+                const int ch = chunk_size(total, nwarps, 32);
+                for (int base = claim(A.work + wc, lane, ch); base < total; base = claim(A.work + wc, lane, ch)) {
+                    if (A.dv_max == 6)
+                        sc_var1_chunk<D, 6, CPT>(A, S, base, min(base + ch, total), cp, lane, s_v1m, s_v1d, s_mf,
+                                                 iscale);
+                    else
+                        sc_var1_chunk<D, 9, CPT>(A, S, base, min(base + ch, total), cp, lane, s_v1m, s_v1d, s_mf,
+                                                 iscale);
+                }
+            }
+        } else if (t == 1) {
+            // general column degrees: one variable per warp pass
+            for (int base = claim(A.work + wc, lane, 8); base < total; base = claim(A.work + wc, lane, 8)) {
+                const int end = min(base + 8, total);
+                int g = base / A.n;
+                unsigned act = group_mask(cp, g, lane);
+                for (int item = base; item < end; ++item) {
+                    const int gi = item / A.n;
+                    if (gi != g) { g = gi; act = group_mask(cp, g, lane); }
+                    if (act)
+                        sc_var1_item<CPT>(A, S, g, item - g * A.n, act, lane, A.Mfix + g * 32 + lane,
+                                          S.Lfix(g * 32 + lane), iscale);
+                }
+            }
+        } else {
+            const int ch = chunk_size(total, nwarps, 32);
+            for (int base = claim(A.work + wc, lane, ch); base < total; base = claim(A.work + wc, lane, ch))
+                sc_var_chunk<CPT>(A, S, base, min(base + ch, total), t, cp, lane, s_w, s_x, iscale);
+        }
+        ++wc;
+    }
+    grid_barrier(A.barrier);
+    stamp(A, ts_k);
+    {   // syndrome phase
+        const int total = G * cblk;
+        for (int base = claim(A.work + wc, lane, kSynChunk); base < total;
+             base = claim(A.work + wc, lane, kSynChunk)) {
+            const int end = min(base + kSynChunk, total);
+            int g = base / cblk;
+            unsigned act = group_mask(cp, g, lane);
+            for (int item = base; item < end; ++item) {
+                const int gi = item / cblk;
+                if (gi != g) { g = gi; act = group_mask(cp, g, lane); }
+                if (act) sc_syncheck_item<CPT>(A, S, g, item - g * cblk, t, act, lane);
+            }
+        }
+        ++wc;
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kDecodeThreads, MBP_SCATTER_MIN_BLOCKS) decode_scatter_kernel(const ScatterArgs A)
+{
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nthreads = gridDim.x * blockDim.x;
+    const int nwarps = nthreads >> 5;
+    const int gw = gtid >> 5;
+    const int cblk = (A.C + 31) / 32;
+    constexpr int CH = Chunk<D>::CH;
+    constexpr int MF = D <= 16 ? (D + 1) * 32 : 1;                 // sweep-1 Mfix table (aliases s_idx)
+    constexpr int SLICE = CH * Chunk<D>::SD > MF ? CH * Chunk<D>::SD : MF;
+    __shared__ int s_idx_all[kDecodeThreads / 32][SLICE];
+    __shared__ unsigned s_w_all[kDecodeThreads / 32][CH > 32 ? CH : 32];
+    __shared__ unsigned s_x_all[kDecodeThreads / 32][CH > 32 ? CH : 32];
+    __shared__ unsigned s_m_all[kDecodeThreads / 32][CH > 32 ? CH : 32];
+    // sweep-1 staging (regular column degree 6 or 9, check degree <= 16)
+    constexpr int V1 = D <= 16 ? 32 * 9 : 1;
+    __shared__ unsigned s_v1m_all[kDecodeThreads / 32][V1];
+    __shared__ uint8_t s_v1d_all[kDecodeThreads / 32][V1];
+    int* s_idx = s_idx_all[warp];
+    unsigned* s_w = s_w_all[warp];
+    unsigned* s_x = s_x_all[warp];
+    unsigned* s_m = s_m_all[warp];
+    unsigned* s_v1m = s_v1m_all[warp];
+    uint8_t* s_v1d = s_v1d_all[warp];
+    int* s_mf = s_idx;   // only used in the sweep-1 variable phase
+
+    // fixed-point scale: |acc| <= Lmax + dv_max * clamp (+ rounding) < 2^30
+    int ex;
+    frexpf(ld_cg(A.Lmax) + (float)A.dv_max * A.clamp + 2.0f, &ex);
+    const int S = min(30 - ex, 40);
+    const float scale = ldexpf(1.0f, S), iscale = ldexpf(1.0f, -S);
+
+    bool cpt = false;
+    int tc = 0;
+    int G = A.G;
+    bool may_compact = A.Gb > 0;
+    int ts_k = 0;
+    int wc = 0;
+    stamp(A, ts_k);
+
+    // fixed-point prior and sweep-1 magnitudes per frame
+    for (int f = gtid; f < A.G * 32; f += nthreads) {
+        A.Lfix[f] = __float2int_rn(A.Lmag[f] * scale);
+        for (int d = 0; d <= A.Dm; ++d)
+            A.Mfix[(size_t)d * A.G * 32 + f] = __float2int_rn(A.Mtab[(size_t)d * A.G * 32 + f] * scale);
+    }
+    // iteration 0: the uncorrected key against all u*m syndromes
+    // (_kernels.py:358-365); keeps the mismatch words for sweeps 1-3
+    {
+        const SL<false> S0{A, A.G};
+        const int total = A.G * cblk;
+        for (int base = claim(A.work + wc, lane, kSynChunk); base < total;
+             base = claim(A.work + wc, lane, kSynChunk))
+            for (int item = base; item < min(base + kSynChunk, total); ++item)
+                sc_syncheck_item<false>(A, S0, item / cblk, item % cblk, 0, kFull, lane);
+        ++wc;
+    }
+
+    int t = 1;
+    int final_t = 0;
+    for (;; ++t) {
+        grid_barrier(A.barrier);
+        stamp(A, ts_k);
+        const int F = G * 32;
+        int* cnt = cpt ? A.cnt_b : A.cnt;
+        const int* cprev = cnt + ((t - 1) & 1) * F;
+        for (int f = gtid; f < F; f += nthreads) {
+            const int c = ld_cg(cprev + f);
+            const int fr = cpt ? ld_cg(A.fid_b + f) : f;
+            if (fr >= 0 && c == 0 && ld_cg(A.iters + fr) < 0) A.iters[fr] = t - 1;
+            cnt[(t & 1) * F + f] = 0;
+            if (may_compact) {
+                const unsigned msk = __ballot_sync(kFull, c != 0);
+                if (lane == 0) {
+                    A.grp_cnt[f >> 5] = __popc(msk);
+                    if (msk) {
+                        atomicAdd(A.ctrl + 2 * t, __popc(msk));
+                        atomicAdd(A.ctrl + 2 * t + 1, 1);
+                    }
+                }
+            }
+        }
+        if (ld_cg(A.any_bad + ((t - 1) & 1)) == 0 || t > A.max_it) {
+            final_t = t - 1;
+            break;
+        }
+        if (gtid == 0) A.any_bad[t & 1] = 0;
+        if (may_compact && t >= 2) {
+            grid_barrier(A.barrier);
+            const int nund = ld_cg(A.ctrl + 2 * t);
+            const int gact = ld_cg(A.ctrl + 2 * t + 1);
+            const int gn = (nund + 31) / 32;
+            if (nund * 2 <= gact * 32 && gn < gact && gn <= A.Gb) {
+                G = sc_compact(A, t, gw, nwarps, gtid, nthreads, lane);
+                cpt = true;
+                tc = t;
+                may_compact = false;
+            }
+        }
+        if (cpt)
+            sc_sweep<D, true>(A, G, t, wc, ts_k, lane, nwarps, s_idx, s_w, s_x, s_m, s_v1m, s_v1d, s_mf, t == tc,
+                              scale, iscale);
+        else
+            sc_sweep<D, false>(A, G, t, wc, ts_k, lane, nwarps, s_idx, s_w, s_x, s_m, s_v1m, s_v1d, s_mf, false,
+                               scale, iscale);
+    }
+
+    if (cpt) grid_barrier(A.barrier);
+    const int* cfin = (cpt ? A.cnt_b : A.cnt) + (final_t & 1) * G * 32;
+    for (int f = gtid; f < A.B; f += nthreads) {
+        const int s = cpt ? ld_cg(A.newslot + f) : f;
+        const int c = s >= 0 ? ld_cg(cfin + s) : 0;
+        const int it = ld_cg(A.iters + f);
+        const bool conv = it >= 0;
+        A.out_conv[f] = conv ? 1 : 0;
+        A.out_iters[f] = conv ? it : A.max_it;
+        A.out_mism[f] = conv ? 0 : c;
+    }
+    if (cpt) scatter_back(A, gw, nwarps, lane);
+    if (gtid == 0) A.sweeps_run[0] = final_t;
+    stamp(A, ts_k);
+}
+
+// Per-frame setup: prior magnitude L = ln((1-e)/e) (init_priors,
+// decoder.py:147-152), the sweep-1 message magnitude for every degree
+// d <= Dm (the reference's sequential product of d-1 factors tanh(L/2),
+// saturation and clamp, in fp64), and the batch maximum of L.
+static __global__ void scatter_setup_kernel(const double* __restrict__ e, int e_stride, int B, int F, int Dm,
+                                     double clamp, float* __restrict__ Lmag, float* __restrict__ Mtab,
+                                     float* __restrict__ Lmax)
+{
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= F) return;
+    double L = 0.0;
+    if (f < B) {
+        const double ef = e[(long long)f * e_stride];
+        L = log((1.0 - ef) / ef);
+    }
+    Lmag[f] = (float)L;
+    const double th = tanh(0.5 * L);
+    double prod = 1.0;
+    Mtab[f] = 0.0f;
+    for (int d = 1; d <= Dm; ++d) {
+        double r = prod >= 1.0 ? clamp : (prod <= -1.0 ? -clamp : 2.0 * atanh(prod));
+        r = r > clamp ? clamp : r;
+        Mtab[(size_t)d * F + f] = f < B ? (float)r : 0.0f;
+        prod *= th;
+    }
+    if (f < B) atomicMax(reinterpret_cast<int*>(Lmax), __float_as_int((float)L));
+}
+
+}  // namespace mbp

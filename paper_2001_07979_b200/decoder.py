@@ -388,7 +388,8 @@ class DecoderWorkspace:
         return slice(int(self.edge_off[l]), int(self.edge_off[l + 1]))
 
     def _device(self, config: DecoderConfig, track: bool) -> BatchDecoder:
-        flags = N.MBP_KEEP_STATE | (N.MBP_RECORD_HISTORY if track else 0)
+        # the fine-grained API reads messages back: explicit-message kernel
+        flags = N.MBP_KEEP_STATE | N.MBP_EXPLICIT_MESSAGES | (N.MBP_RECORD_HISTORY if track else 0)
         shape_key = (config.precision, config.combining_mode)
         if self._dec is None or self._dec_key != shape_key:
             self._dec = BatchDecoder(self.ensemble, 1, config, flags=flags)
