@@ -454,7 +454,10 @@ __device__ __forceinline__ void var_chunk_regular(const DecodeArgs<Real>& A, con
 // Move lane values of an interleaved [G][X][32] array into the compacted
 // layout: dst[g'][x][l'] = src[s/32][x][s%32], s = src_b[g'*32 + l'].
 // The source reads are scattered (one sector per lane), so each warp item
-// keeps XU independent loads in flight.
+// keeps XU independent loads in flight.  They go through L1 (ld.ca): lanes
+// of one source group share sectors, and no source array changes during
+// the compaction (L1 is invalidated by the __threadfence of every grid
+// barrier, so no stale line survives from an earlier phase).
 template <class T>
 __device__ __forceinline__ void move_lanes(const T* src, T* dst, long long X, int Gn, const int* src_b,
                                            int gw, int nw, int lane)
@@ -469,7 +472,7 @@ __device__ __forceinline__ void move_lanes(const T* src, T* dst, long long X, in
         T* dp = dst + ((size_t)g2 * X + x0) * 32 + lane;
         T v[XU];
 #pragma unroll
-        for (int k = 0; k < XU; ++k) v[k] = (s >= 0 && x0 + k < X) ? ld_cg(sp + k * 32) : T(0);
+        for (int k = 0; k < XU; ++k) v[k] = (s >= 0 && x0 + k < X) ? __ldca(sp + k * 32) : T(0);
 #pragma unroll
         for (int k = 0; k < XU; ++k)
             if (x0 + k < X) dp[k * 32] = v[k];
@@ -489,7 +492,7 @@ __device__ __forceinline__ void move_bits(const unsigned* src, unsigned* dst, lo
         const unsigned* sp = src + (s >= 0 ? (size_t)(s >> 5) * X : 0) + x0;
         unsigned w[XU];
 #pragma unroll
-        for (int k = 0; k < XU; ++k) w[k] = (s >= 0 && x0 + k < X) ? ld_cg(sp + k) : 0u;
+        for (int k = 0; k < XU; ++k) w[k] = (s >= 0 && x0 + k < X) ? __ldca(sp + k) : 0u;
         unsigned mine = 0;
 #pragma unroll
         for (int k = 0; k < XU; ++k) {

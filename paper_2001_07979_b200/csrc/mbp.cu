@@ -107,8 +107,7 @@ struct mbp_workspace {
         sweeps, ts, work, tmp_in,
         c2v_b, post_b, v2c_b, Lmag_b, noisy_b, syn_b, hard_b, cnt_b, fid_b, src_b, newslot, grp_cnt, ctrl, tmp_out, tmp_conv, tmp_iters, tmp_mism, tmp_e;
     // scatter path (scatter.cuh)
-    DevBuf sc_post, sc_acc, sc_mis, sc_Mtab, sc_Lfix, sc_Mfix, sc_Lmax,
-        sc_post_b, sc_acc_b, sc_Mtab_b, sc_Lfix_b, sc_mis_b;
+    DevBuf sc_vb, sc_mis, sc_Mtab, sc_Lfix, sc_Mfix, sc_Lmax, sc_vb_b, sc_Mtab_b, sc_Lfix_b, sc_mis_b;
     bool scatter = false;   // path of the current configuration
     int ts_cap = 0;
     int Gb = 0;        // compaction capacity (groups), 0 = disabled
@@ -279,6 +278,7 @@ static bool scatter_eligible(const mbp_ensemble* ens, const mbp_decoder_config& 
 {
     return cfg.precision == MBP_FP32_PHI && cfg.combining_mode == MBP_JOINT_GRAPH && cfg.damping == 0.0 &&
            !(cfg.flags & MBP_EXPLICIT_MESSAGES) && scatter_degree(ens->Ds) != 0 &&
+           (double)ens->n * mbp::kVB * 4 < 4294967296.0 &&   // 32-bit byte offsets of variable blocks
            (double)ens->dmax_v * cfg.llr_clamp <= 1024.0;
 }
 
@@ -330,11 +330,11 @@ static int ws_alloc(mbp_workspace* ws)
     {   // scatter-path state (sized 0 when the explicit kernel runs)
         const bool sc = ws->scatter;
         const size_t G = ws->G, Gb = ws->Gb, n = ens->n, C = ens->C, Dm1 = ens->Ds + 1;
-        if ((rc = fit(ws->sc_post, sc ? 2 * G * n * 32 * 4 : 0)) || (rc = fit(ws->sc_acc, sc ? G * n * 32 * 4 : 0)) ||
+        if ((rc = fit(ws->sc_vb, sc ? G * n * mbp::kVB * 4 : 0)) ||
             (rc = fit(ws->sc_mis, sc ? G * C * 4 : 0)) || (rc = fit(ws->sc_Mtab, sc ? Dm1 * G * 32 * 4 : 0)) ||
             (rc = fit(ws->sc_Lfix, sc ? G * 32 * 4 : 0)) || (rc = fit(ws->sc_Mfix, sc ? Dm1 * G * 32 * 4 : 0)) ||
-            (rc = fit(ws->sc_Lmax, sc ? 4 : 0)) || (rc = fit(ws->sc_post_b, sc ? 2 * Gb * n * 32 * 4 : 0)) ||
-            (rc = fit(ws->sc_acc_b, sc ? Gb * n * 32 * 4 : 0)) || (rc = fit(ws->sc_Mtab_b, sc ? Dm1 * Gb * 32 * 4 : 0)) ||
+            (rc = fit(ws->sc_Lmax, sc ? 4 : 0)) || (rc = fit(ws->sc_vb_b, sc ? Gb * n * mbp::kVB * 4 : 0)) ||
+            (rc = fit(ws->sc_Mtab_b, sc ? Dm1 * Gb * 32 * 4 : 0)) ||
             (rc = fit(ws->sc_Lfix_b, sc ? Gb * 32 * 4 : 0)) || (rc = fit(ws->sc_mis_b, sc ? Gb * C * 4 : 0)))
             return rc;
         if (sc && (rc = fit(ws->post_b, 0))) return rc;
@@ -481,20 +481,20 @@ static __global__ void fill_post_prior_kernel(const unsigned* __restrict__ noisy
 
 // scatter-path state is kept in the noisy-relative domain (scatter.cuh):
 // post' = (-1)^y post.  Prior fill and readback convert.
-static __global__ void fill_rel_prior_kernel(const float* __restrict__ L, int G, int n, float* __restrict__ post)
+static __global__ void fill_rel_prior_kernel(const float* __restrict__ L, int G, int n, float* __restrict__ vb)
 {
     const long long total = (long long)G * n * 32;
     for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < total;
          k += (long long)gridDim.x * blockDim.x)
-        post[k] = L[(k >> 5) / n * 32 + (k & 31)];
+        vb[(k >> 5) * mbp::kVB + (k & 31)] = L[(k >> 5) / n * 32 + (k & 31)];   // line 0 of the block
 }
 
-static __global__ void gather_rel_post_kernel(const float* __restrict__ post_g, const unsigned* __restrict__ noisy_g,
+static __global__ void gather_rel_post_kernel(const float* __restrict__ vb_g, const unsigned* __restrict__ noisy_g,
                                               int n, int lane, double* __restrict__ dst)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) {
-        const double v = post_g[(long long)i * 32 + lane];
+        const double v = vb_g[(long long)i * mbp::kVB + lane] * 0.69314718055994530942;   // log2 -> natural units
         dst[i] = ((noisy_g[i] >> lane) & 1u) ? -v : v;
     }
 }
@@ -528,7 +528,7 @@ static int decode_chunk_scatter(mbp_workspace* ws, const uint8_t* noisy, const u
     if (cfg.flags & MBP_KEEP_STATE) {
         // slot 0 holds the prior (+L in the noisy-relative domain) for frames
         // that stop at iteration 0
-        fill_rel_prior_kernel<<<1024, 256, 0, s>>>(ws->Lmag.as<float>(), G, ens->n, ws->sc_post.as<float>());
+        fill_rel_prior_kernel<<<1024, 256, 0, s>>>(ws->Lmag.as<float>(), G, ens->n, ws->sc_vb.as<float>());
         MBP_CUDA(cudaGetLastError());
     }
     MBP_CUDA(cudaMemsetAsync(ws->cnt.p, 0, 2 * (size_t)F * 4, s));
@@ -551,14 +551,14 @@ static int decode_chunk_scatter(mbp_workspace* ws, const uint8_t* noisy, const u
     A.var_ptr = ens->var_ptr.as<int>(); A.var_chk = ens->var_chk.as<int>();
     A.dv_max = ens->dmax_v; A.var_ptr_regular = ens->dv_reg == ens->dmax_v; A.Dm = Dm;
     A.G = G; A.B = B;
-    A.post = ws->sc_post.as<float>(); A.acc = ws->sc_acc.as<int>(); A.c2v = ws->c2v.as<float>();
+    A.vb = ws->sc_vb.as<float>(); A.c2v = ws->c2v.as<float>();
     A.Lmag = ws->Lmag.as<float>(); A.Mtab = ws->sc_Mtab.as<float>();
     A.Lfix = ws->sc_Lfix.as<int>(); A.Mfix = ws->sc_Mfix.as<int>();
     A.noisy_w = ws->noisy_w.as<unsigned>(); A.syn_w = ws->syn_w.as<unsigned>(); A.mis_w = ws->sc_mis.as<unsigned>();
     A.hard_w = ws->hard_w.as<unsigned>(); A.hist_w = record ? ws->hist_w.as<unsigned>() : nullptr;
     A.cnt = ws->cnt.as<int>();
     A.Gb = G >= 2 ? std::min(ws->Gb, (G + 1) / 2) : 0;
-    A.post_b = ws->sc_post_b.as<float>(); A.acc_b = ws->sc_acc_b.as<int>(); A.c2v_b = ws->c2v_b.as<float>();
+    A.vb_b = ws->sc_vb_b.as<float>(); A.c2v_b = ws->c2v_b.as<float>();
     A.Lmag_b = ws->Lmag_b.as<float>(); A.Mtab_b = ws->sc_Mtab_b.as<float>(); A.Lfix_b = ws->sc_Lfix_b.as<int>();
     A.noisy_b = ws->noisy_b.as<unsigned>(); A.syn_b = ws->syn_b.as<unsigned>(); A.mis_b = ws->sc_mis_b.as<unsigned>();
     A.hard_b = ws->hard_b.as<unsigned>(); A.cnt_b = ws->cnt_b.as<int>(); A.fid_b = ws->fid_b.as<int>();
@@ -569,7 +569,10 @@ static int decode_chunk_scatter(mbp_workspace* ws, const uint8_t* noisy, const u
     A.ts = ws->ts_cap ? ws->ts.as<unsigned long long>() : nullptr; A.ts_cap = ws->ts_cap;
     A.Lmax = ws->sc_Lmax.as<float>();
     A.out_conv = conv; A.out_iters = iters; A.out_mism = mism;
-    A.max_it = cfg.max_iterations; A.clamp = (float)cfg.llr_clamp; A.sat = ens->sat;
+    // the scatter kernel works in log2 units (scatter.cuh)
+    A.max_it = cfg.max_iterations;
+    A.clamp = (float)((double)(float)cfg.llr_clamp * 1.4426950408889634074);
+    A.sat = (float)((double)ens->sat * 1.4426950408889634074);
     if ((rc = dispatch_scatter(ws, A, s))) return rc;
     if ((rc = launch_words_to_rows(ws->hard_w.as<unsigned>(), ens->n, B, G, 1, ens->n, nb, corrected, nb, s)))
         return rc;
@@ -804,8 +807,7 @@ int mbp_workspace_read_posterior(mbp_workspace* ws, int64_t frame, double* poste
         int it = -1;
         MBP_CUDA(cudaMemcpy(&it, ws->iters.as<int>() + frame, 4, cudaMemcpyDeviceToHost));
         const int last = it >= 0 ? it : ws->cfg.max_iterations;
-        const size_t Gc = (ws->last_B + 31) / 32;
-        const float* base = ws->sc_post.as<float>() + ((size_t)(last & 1) * Gc + g) * ens->n * 32;
+        const float* base = ws->sc_vb.as<float>() + g * ens->n * mbp::kVB + (size_t)(last & 1) * 32;
         DevBuf tmp;
         int rc;
         if ((rc = tmp.alloc((size_t)ens->n * 8))) return rc;

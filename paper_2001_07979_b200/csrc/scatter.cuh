@@ -35,6 +35,8 @@
 //    parity), and every sweep-1 message of check j is the same value
 //    (-1)^s_j M_{d_j}: the check phase needs no per-edge key bits.  The hard
 //    decision is post_b < 0  <=>  (y_b ? post'_b > 0 : post'_b < 0).
+//  * LLRs are carried in log2 units (x log2 e: u = 2^-|x| and the message
+//    log2(S/D) need no scaling); posteriors are converted back on readback.
 //  * Eq. 6 in (S, Delta) form: with u = e^-|x|, tanh(|x|/2) = (1-u)/(1+u);
 //    for a set of edges A = prod(1+u), B = prod(1-u), S = A + B, D = A - B
 //    combine as (S, D) x (1, u) = (S + uD, D + uS) -- only additions of
@@ -44,8 +46,10 @@
 //    and suffix pairs; 3 MUFU per edge (ex2, 2 x lg2).
 //
 // Layout as in kernels.cuh (lane = frame, groups of 32 frames), plus
-//   post[2][Gc][n][32] f32    post_s lives in slot s & 1
-//   acc[Gc][n][32]     s32    fixed-point posterior being accumulated
+//   vb[Gc][n][3][32]   one 384-byte block per variable and group: line 0/1 =
+//                      post' of even/odd sweeps (f32), line 2 = acc (s32), so
+//                      one address per edge serves the posterior gathers and
+//                      the accumulation (immediate offsets +128 / +256)
 //   mis_w[Gc][C]       u32    iteration-0 mismatch words
 //   Mtab[Dm+1][Fc]     f32    sweep-1 message magnitude per degree and frame
 // (Gc = groups of the layout's allocation, Fc = 32 Gc).
@@ -56,10 +60,15 @@
 namespace mbp {
 
 constexpr int kStoreFrom = 3;   // c2v_t is stored for t >= kStoreFrom
+constexpr int kVB = 96;         // 32-bit words per variable block (3 lines)
 
 #ifndef MBP_SCATTER_MIN_BLOCKS
 #define MBP_SCATTER_MIN_BLOCKS 4
 #endif
+// resident blocks per SM: 64 registers up to degree 8; wider rows keep two
+// rows' gathers in flight and need 128 (no spills)
+template <int D>
+constexpr int scatter_min_blocks() { return D <= 8 ? MBP_SCATTER_MIN_BLOCKS : 2; }
 
 struct ScatterArgs {
     // graph
@@ -74,9 +83,8 @@ struct ScatterArgs {
     int Dm;                           // Mtab degree bound (= Ds)
     // primary layout
     int G, B;
-    float* post;
-    int* acc;
-    float* c2v;
+    float* vb;                        // [G][n][3][32]
+    float* c2v;                       // [G][slots][32]
     const float* Lmag;                // [F]
     const float* Mtab;                // [Dm+1][F]
     int* Lfix;                        // [F]   round(L * 2^S), written by the kernel
@@ -89,8 +97,7 @@ struct ScatterArgs {
     int* cnt;
     // compacted layout (capacity Gb groups)
     int Gb;
-    float* post_b;
-    int* acc_b;
+    float* vb_b;
     float* c2v_b;
     float* Lmag_b;
     float* Mtab_b;
@@ -129,11 +136,8 @@ struct SL {
     const ScatterArgs& A;
     int G;                            // groups of the current layout
     __device__ __forceinline__ int Gc() const { return CPT ? A.Gb : A.G; }
-    __device__ __forceinline__ float* post(int sweep) const
-    {
-        return (CPT ? A.post_b : A.post) + (size_t)(sweep & 1) * Gc() * A.n * 32;
-    }
-    __device__ __forceinline__ int* acc() const { return CPT ? A.acc_b : A.acc; }
+    // lane's word of variable i's block in group g
+    __device__ __forceinline__ float* vrow(size_t w, int lane) const { return (CPT ? A.vb_b : A.vb) + w * kVB + lane; }
     __device__ __forceinline__ float* c2v() const { return CPT ? A.c2v_b : A.c2v; }
     __device__ __forceinline__ unsigned* hard_w() const { return CPT ? A.hard_b : A.hard_w; }
     __device__ __forceinline__ unsigned* mis() const { return CPT ? A.mis_b : A.mis_w; }
@@ -147,21 +151,29 @@ struct SL {
     __device__ __forceinline__ int Lfix(int s) const { return ld_cg((CPT ? A.Lfix_b : A.Lfix) + s); }
 };
 
+__device__ __forceinline__ const float* byte_off(const float* p, unsigned off)
+{
+    return reinterpret_cast<const float*>(reinterpret_cast<const char*>(p) + off);
+}
+
 // ptxas branches around a lane-predicated REDG (BSSY/BRA/BSYNC per edge), so
 // dead lanes add 0 instead: the warp's line request is issued either way.
-__device__ __forceinline__ void red_add(int* p, int v)
+__device__ __forceinline__ void red_add(const float* p, int v)
 {
     asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
 
 // ---------------------------------------------------------------------------
-// Eq. 6, (S, Delta) form (header comment).  Slots k >= d (PAD) and inputs
-// with |x| >= sat (where the reference's float64 tanh(x/2) is exactly 1.0)
-// get u = 0, the neutral factor (1, 0); a message whose other factors are
-// all neutral has D = 0 -> ln(S/0) = inf -> +-clamp, the reference's
-// `prod >= 1.0` branch (_kernels.py:249-252).
+// Eq. 6, (S, Delta) form (header comment), in log2 units: inputs are the raw
+// differences x = post' - c2v' (the clamp is applied here as min(|x|, clamp),
+// the sign taken from x), u = 2^-|x|, output log2(S/D).  Slots k >= d (PAD)
+// and, when SAT, inputs with |x| >= sat (where the reference's float64
+// tanh(x/2) is exactly 1.0) get u = 0, the neutral factor (1, 0); a message
+// whose other factors are all neutral has D = 0 -> log2(S/0) = inf -> +-clamp,
+// the reference's `prod >= 1.0` branch (_kernels.py:249-252).  With
+// clamp < sat no clamped input can reach sat, so SAT = false is exact.
 // ---------------------------------------------------------------------------
-template <int DD, bool PAD>
+template <int DD, bool PAD, bool SAT>
 __device__ __forceinline__ void rule_sd(const float (&x)[DD], int d, unsigned flip, float clamp, float sat,
                                         float (&out)[DD])
 {
@@ -171,9 +183,9 @@ __device__ __forceinline__ void rule_sd(const float (&x)[DD], int d, unsigned fl
 #pragma unroll
     for (int k = 0; k < DD; ++k) {
         const bool in = !PAD || k < d;
-        const float a = fabsf(x[k]);
-        const float u = ex2_approx(-1.44269504088896341f * a);
-        uu[k] = (in && a < sat) ? u : 0.0f;
+        const float a = fminf(fabsf(x[k]), clamp);
+        const float u = ex2_approx(-a);
+        uu[k] = (in && (!SAT || a < sat)) ? u : 0.0f;
         sb[k] = in ? (__float_as_uint(x[k]) & 0x80000000u) : 0u;
         tot ^= sb[k];
     }
@@ -192,7 +204,7 @@ __device__ __forceinline__ void rule_sd(const float (&x)[DD], int d, unsigned fl
     for (int k = 0; k < DD; ++k) {
         const float eS = fmaf(pS, sS[k], pD * sD[k]);
         const float eD = fmaf(pS, sD[k], pD * sS[k]);
-        const float mag = fminf((lg2_approx(eS) - lg2_approx(eD)) * 0.69314718055994531f, clamp);
+        const float mag = fminf(lg2_approx(eS) - lg2_approx(eD), clamp);
         out[k] = __uint_as_float(__float_as_uint(mag) | (tot ^ sb[k]));
         const float S2 = fmaf(pD, uu[k], pS);
         pD = fmaf(pS, uu[k], pD);
@@ -201,71 +213,59 @@ __device__ __forceinline__ void rule_sd(const float (&x)[DD], int d, unsigned fl
 }
 
 // ---------------------------------------------------------------------------
-// check phase: check j of group g at sweep t >= 2.  srow = the row's variable
-// ids (staged), d its degree (<= DD), mis/syn words of the row, M1 = this
-// lane's sweep-1 magnitude for degree d, qrow = c2v_{t-1} row base (explicit
-// base only).  Computes c2v_t, adds it into acc, stores it for t >= kStoreFrom.
+// check phase (t >= 2).  A warp owns a claimed chunk of rows (checks) of one
+// or two groups; lane = frame.  Row variable offsets are staged in shared
+// memory as byte offsets of variable blocks (pad slots -> 0: they read
+// variable 0 and add 0 to it, so no load needs a per-slot predicate).
+// The base message c2v'_{s0-1} is rebuilt from the mismatch bit while
+// t <= kStoreFrom (s0 = 2), read from the stored row otherwise (s0 = t); the
+// chain c2v'_s = rule(clamp(post'_{s-1} - c2v'_{s-1})), s = s0..t, ends in
+// c2v'_t, which is added into acc (and stored when t >= kStoreFrom).  The
+// first gather (post'_{s0-1}) of the next row is issued before the current
+// row's rule (software pipeline).  FULL: every lane of the group is live.
 // ---------------------------------------------------------------------------
-template <int DD, bool PAD, bool CPT>
-__device__ __forceinline__ void sc_check_item(const ScatterArgs& A, const SL<CPT>& S, int g, int j, int t,
-                                              bool live, int lane, const int* srow, int d, unsigned misword,
-                                              float M1, const float* qrow, float scale)
+template <int D, int DD, bool PAD, bool FULL, bool SAT, bool CPT>
+__device__ __forceinline__ void sc_row(const ScatterArgs& A, const SL<CPT>& S, const float (&p)[D], int d,
+                                       unsigned sj, float M1, const unsigned* soff, bool live, int t,
+                                       const float* gb, const float* qrow, float* crow, float scale)
 {
-    const unsigned sj = (misword >> lane) & 1u;        // relative-domain syndrome sign
-    const size_t gl = (size_t)g * A.n * 32 + lane;     // element (g, 0, lane)
-    unsigned off[DD];
-#pragma unroll
-    for (int k = 0; k < DD; ++k) off[k] = (!PAD || k < d) ? (unsigned)srow[k] * 32u : 0u;
+    const bool lv = FULL || live;
     const bool explicit_base = t > kStoreFrom;
     float c[DD];
     if (!explicit_base) {
-        const float c1 = sj ? -M1 : M1;                 // c2v'_1, the same on every edge
+        const float c1 = sj ? -M1 : M1;          // c2v'_1, the same on every edge of the row
 #pragma unroll
         for (int k = 0; k < DD; ++k) c[k] = c1;
     } else {
 #pragma unroll
-        for (int k = 0; k < DD; ++k) c[k] = ld_cg_if(qrow + k * 32, live && (!PAD || k < d));
+        for (int k = 0; k < DD; ++k) c[k] = ld_cg_if(qrow + k * 32, lv && (!PAD || k < d));
     }
-    // c2v'_s from c2v'_{s-1} and post'_{s-1}, s = first..t
-    for (int s = explicit_base ? t : 2; s <= t; ++s) {
-        const float* pp = S.post(s - 1) + gl;
-        float x[DD];
+    float x[DD];
+#pragma unroll
+    for (int k = 0; k < DD; ++k) x[k] = p[k] - c[k];
+    rule_sd<DD, PAD, SAT>(x, d, sj, A.clamp, A.sat, c);
+    for (int s = (explicit_base ? t : 2) + 1; s <= t; ++s) {
+        const float* gs = gb + ((s - 1) & 1) * 32;   // post'_{s-1} line
 #pragma unroll
         for (int k = 0; k < DD; ++k) {
-            const float p = ld_cg_if(pp + off[k], live && (!PAD || k < d));
-            x[k] = clampr(p - c[k], A.clamp);
+            const float* q = byte_off(gs, soff[k]);
+            x[k] = (FULL ? ld_cg(q) : ld_cg_if(q, live)) - c[k];
         }
-        rule_sd<DD, PAD>(x, d, sj, A.clamp, A.sat, c);
+        rule_sd<DD, PAD, SAT>(x, d, sj, A.clamp, A.sat, c);
     }
-    int* accg = S.acc() + gl;
+    if (t >= kStoreFrom) {
+        // padded-ELL rows own Ds slots, so pad slots may be written
+#pragma unroll
+        for (int k = 0; k < DD; ++k) st_if(crow + k * 32, c[k], lv);
+    }
 #pragma unroll
     for (int k = 0; k < DD; ++k) {
         const int v = __float2int_rn(c[k] * scale);
-        red_add(accg + off[k], (live && (!PAD || k < d)) ? v : 0);   // pads: off = 0
-    }
-    if (t >= kStoreFrom) {
-        float* crow = S.c2v() + ((size_t)g * A.slots + (size_t)j * A.Ds) * 32 + lane;
-#pragma unroll
-        for (int k = 0; k < DD; ++k) st_if(crow + k * 32, c[k], live && (!PAD || k < d));
+        red_add(byte_off(gb, soff[k]) + 64, (lv && (!PAD || k < d)) ? v : 0);   // acc line
     }
 }
 
-template <int D, bool CPT>
-__device__ __forceinline__ void sc_check_dispatch(const ScatterArgs& A, const SL<CPT>& S, int g, int j, int t,
-                                                  bool live, int lane, const int* srow, int d, unsigned misword,
-                                                  float M1, const float* qrow, float scale)
-{
-    // the row degree is warp-uniform: exact-degree code for the two most
-    // common degrees (D and D-1), padded code for the rest
-    if (d == D)
-        sc_check_item<D, false, CPT>(A, S, g, j, t, live, lane, srow, d, misword, M1, qrow, scale);
-    else if (D > 1 && d == D - 1)
-        sc_check_item<(D > 1 ? D - 1 : 1), false, CPT>(A, S, g, j, t, live, lane, srow, d, misword, M1, qrow, scale);
-    else
-        sc_check_item<D, true, CPT>(A, S, g, j, t, live, lane, srow, d, misword, M1, qrow, scale);
-}
-
-// c2v_{t-1} row base for lane `lane` of group g (explicit base only); the
+// c2v'_{t-1} row base for lane `lane` of group g (explicit base only); the
 // first sweep after a compaction reads it in place from the frame's
 // original lane of the primary layout.
 template <bool CPT>
@@ -279,10 +279,63 @@ __device__ __forceinline__ const float* sc_c2v_in_base(const ScatterArgs& A, con
     return S.c2v() + (size_t)g * A.slots * 32 + lane;
 }
 
+// rows [r0, r1) of the staged chunk, all in group g (first row j0)
+template <int D, bool FULL, bool SAT, bool CPT>
+__device__ __forceinline__ void sc_span(const ScatterArgs& A, const SL<CPT>& S, int g, int j0, int r0, int r1, int t,
+                                        unsigned act, int lane, const unsigned* s_off, const unsigned* s_m,
+                                        const int* s_d, const float* s_m1, bool first, float scale)
+{
+    constexpr int SD = Chunk<D>::SD;
+    const bool live = (act >> lane) & 1u;
+    const bool explicit_base = t > kStoreFrom;
+    const float* gb = S.vrow((size_t)g * A.n, lane);
+    const float* qb = explicit_base ? sc_c2v_in_base<CPT>(A, S, g, lane, first) : nullptr;
+    // first gather: post'_{s0-1}
+    const float* gf = gb + (((explicit_base ? t : 2) - 1) & 1) * 32;
+    float pn[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        const float* q = byte_off(gf, s_off[r0 * SD + k]);
+        pn[k] = FULL ? ld_cg(q) : ld_cg_if(q, live);
+    }
+    int dn = s_d[r0];
+    for (int r = r0; r < r1; ++r) {
+        float p[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) p[k] = pn[k];
+        const int d = dn;
+        if (r + 1 < r1) {
+            dn = s_d[r + 1];
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                const float* q = byte_off(gf, s_off[(r + 1) * SD + k]);
+                pn[k] = FULL ? ld_cg(q) : ld_cg_if(q, live);
+            }
+        }
+        const unsigned sj = (s_m[r] >> lane) & 1u;
+        float M1 = 0.0f;
+        if (!explicit_base) {
+            if constexpr (D <= 16) M1 = s_m1[d * 32 + lane];
+            else M1 = S.M1(d, g * 32 + lane);
+        }
+        const unsigned* soff = s_off + r * SD;
+        const int j = j0 + (r - r0);
+        const float* qrow = explicit_base ? qb + (size_t)j * A.Ds * 32 : nullptr;
+        float* crow = t >= kStoreFrom ? S.c2v() + ((size_t)g * A.slots + (size_t)j * A.Ds) * 32 + lane : nullptr;
+        if (d == D)
+            sc_row<D, D, false, FULL, SAT, CPT>(A, S, p, d, sj, M1, soff, live, t, gb, qrow, crow, scale);
+        else if (D > 1 && d == D - 1)
+            sc_row<D, (D > 1 ? D - 1 : 1), false, FULL, SAT, CPT>(A, S, p, d, sj, M1, soff, live, t, gb, qrow,
+                                                                  crow, scale);
+        else
+            sc_row<D, D, true, FULL, SAT, CPT>(A, S, p, d, sj, M1, soff, live, t, gb, qrow, crow, scale);
+    }
+}
+
 template <int D, bool CPT>
 __device__ __forceinline__ void sc_check_chunk(const ScatterArgs& A, const SL<CPT>& S, int base, int end, int t,
-                                               const int* cprev, int lane, int* s_idx, unsigned* s_w,
-                                               unsigned* s_m, int* s_d, bool first, float scale)
+                                               const int* cprev, int lane, unsigned* s_off, unsigned* s_m,
+                                               int* s_d, float* s_m1, bool first, float scale)
 {
     constexpr int SD = Chunk<D>::SD;
     const int rows = end - base;
@@ -294,28 +347,34 @@ __device__ __forceinline__ void sc_check_chunk(const ScatterArgs& A, const SL<CP
         s_m[lane] = ld_cg(S.mis() + item);     // mis index == item (g*C + j)
         const int* row = A.chk_ell + (size_t)j * A.Ds;
 #pragma unroll
-        for (int k = 0; k < D; ++k)
-            if (k < d) s_idx[lane * SD + k] = ld_ro(row + k);
+        for (int k = 0; k < D; ++k) s_off[lane * SD + k] = k < d ? (unsigned)ld_ro(row + k) * (kVB * 4u) : 0u;
     }
     __syncwarp();
-    int g = base / A.C;
-    int j = base - g * A.C;
-    unsigned act = group_mask(cprev, g, lane);
-    const float* qb = t > kStoreFrom ? sc_c2v_in_base<CPT>(A, S, g, lane, first) : nullptr;
-    for (int r = 0; r < rows; ++r) {
+    int r = 0;
+    while (r < rows) {
+        const int item = base + r;
+        const int g = item / A.C;
+        const int j0 = item - g * A.C;
+        const int span = min(rows - r, A.C - j0);
+        const unsigned act = group_mask(cprev, g, lane);
         if (act) {
-            const int d = s_d[r];
-            const float M1 = t <= kStoreFrom ? S.M1(d, g * 32 + lane) : 0.0f;
-            const float* qrow = qb ? qb + (size_t)j * A.Ds * 32 : nullptr;
-            sc_check_dispatch<D, CPT>(A, S, g, j, t, (act >> lane) & 1u, lane, s_idx + r * SD, d, s_m[r], M1,
-                                      qrow, scale);
+            if constexpr (D <= 16) {
+                if (t <= kStoreFrom) {
+#pragma unroll
+                    for (int dd = 0; dd <= D; ++dd) s_m1[dd * 32 + lane] = S.M1(dd, g * 32 + lane);
+                    __syncwarp();
+                }
+            }
+            // fast variant: every lane live and no input can saturate
+            if (act == kFull && A.clamp < A.sat)
+                sc_span<D, true, false, CPT>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d, s_m1, first,
+                                             scale);
+            else
+                sc_span<D, false, true, CPT>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d, s_m1, first,
+                                             scale);
+            __syncwarp();
         }
-        if (++j == A.C && r + 1 < rows) {
-            j = 0;
-            ++g;
-            act = group_mask(cprev, g, lane);
-            qb = t > kStoreFrom ? sc_c2v_in_base<CPT>(A, S, g, lane, first) : nullptr;
-        }
+        r += span;
     }
     __syncwarp();
 }
@@ -324,10 +383,11 @@ __device__ __forceinline__ void sc_check_chunk(const ScatterArgs& A, const SL<CP
 // variable phases
 // ---------------------------------------------------------------------------
 
-// sweep 1: post_1 = prior + sum of the sweep-1 messages, in fixed point
-// (exactly what the check-side accumulation of later sweeps computes).
-// Lanes load the variable's check ids, mismatch words and degrees, then the
-// warp walks them with shuffles.  Also arms acc with the prior for sweep 2.
+// Sweep 1: post'_1 = L + sum of the sweep-1 messages (-1)^s_j M_{d_j}, in
+// fixed point (what the check-side accumulation of later sweeps computes);
+// arms acc with the prior for sweep 2.  General column degrees: lanes load
+// the variable's check ids, mismatch words and degrees, the warp walks them
+// with shuffles.
 template <bool CPT>
 __device__ __forceinline__ void sc_var1_item(const ScatterArgs& A, const SL<CPT>& S, int g, int i, unsigned act,
                                              int lane, const int* Mfix, int Lf, float iscale)
@@ -354,8 +414,9 @@ __device__ __forceinline__ void sc_var1_item(const ScatterArgs& A, const SL<CPT>
             a += ((mw >> lane) & 1u) ? -mf : mf;
         }
     }
-    st_if(S.post(1) + w * 32 + lane, (float)a * iscale, live);
-    if (live) S.acc()[w * 32 + lane] = Lf;
+    float* vr = S.vrow(w, lane);
+    st_if(vr + 32, (float)a * iscale, live);
+    if (live) reinterpret_cast<int*>(vr)[64] = Lf;
     const unsigned neg = __ballot_sync(kFull, y ? a > 0 : a < 0);
     if (lane == 0) {
         // the iteration-0 decision of every frame is its noisy key
@@ -365,10 +426,10 @@ __device__ __forceinline__ void sc_var1_item(const ScatterArgs& A, const SL<CPT>
     }
 }
 
-// Sweep 1 for a regular column degree DV <= 16: one chunk of <= 32
-// variables.  The chunk's check ids, mismatch words and degrees are staged
-// in shared memory with independent loads (two dependent round trips per
-// chunk), the lane's Mfix row per degree sits in a shared table.
+// Sweep 1 for a regular column degree DV (6 or 9), check degree D <= 16: one
+// chunk of <= 32 variables.  The chunk's mismatch words and check degrees
+// are staged in shared memory with independent loads (two dependent round
+// trips per chunk), the lane's Mfix row per degree sits in a shared table.
 template <int D, int DV, bool CPT>
 __device__ __forceinline__ void sc_var1_chunk(const ScatterArgs& A, const SL<CPT>& S, int base, int end,
                                               const int* cprev, int lane, unsigned* s_mis, uint8_t* s_deg,
@@ -410,11 +471,11 @@ __device__ __forceinline__ void sc_var1_chunk(const ScatterArgs& A, const SL<CPT
                     const int mf = s_mf[s_deg[v * DV + k] * 32 + lane];
                     a += ((mw >> lane) & 1u) ? -mf : mf;
                 }
-                st_if(S.post(1) + w * 32 + lane, (float)a * iscale, live);
-                if (live) S.acc()[w * 32 + lane] = Lf;
+                float* vr = S.vrow(w, lane);
+                st_if(vr + 32, (float)a * iscale, live);
+                if (live) reinterpret_cast<int*>(vr)[64] = Lf;
                 const unsigned neg = __ballot_sync(kFull, y ? a > 0 : a < 0);
                 if (lane == 0) {
-                    // the iteration-0 decision of every frame is its noisy key
                     const unsigned hw = (neg & act) | (yw & ~act);
                     S.hard_w()[w] = hw;
                     if (A.hist_w) A.hist_w[((size_t)1 * A.G) * A.n + w] = hw;
@@ -427,7 +488,7 @@ __device__ __forceinline__ void sc_var1_chunk(const ScatterArgs& A, const SL<CPT
     __syncwarp();
 }
 
-// sweep t >= 2: acc -> post_t, hard decision, re-arm acc with the prior.
+// sweep t >= 2: acc -> post'_t, hard decision, re-arm acc with the prior.
 template <bool CPT>
 __device__ __forceinline__ void sc_var_chunk(const ScatterArgs& A, const SL<CPT>& S, int base, int end, int t,
                                              const int* cprev, int lane, unsigned* s_w, unsigned* s_old,
@@ -439,8 +500,7 @@ __device__ __forceinline__ void sc_var_chunk(const ScatterArgs& A, const SL<CPT>
         s_old[lane] = ld_cg(S.hard_w() + base + lane);
     }
     __syncwarp();
-    float* postt = S.post(t);
-    int* acc = S.acc();
+    const int slot = (t & 1) * 32;
     int r = 0;
     while (r < rows) {
         const int item = base + r;
@@ -457,15 +517,16 @@ __device__ __forceinline__ void sc_var_chunk(const ScatterArgs& A, const SL<CPT>
 #pragma unroll
                 for (int v = 0; v < U; ++v) {
                     const size_t w = (size_t)item + k0 + v;
-                    a[v] = (k0 + v < span && live) ? ld_cg(acc + w * 32 + lane) : 0;
+                    a[v] = (k0 + v < span && live) ? ld_cg(reinterpret_cast<const int*>(S.vrow(w, lane)) + 64) : 0;
                 }
 #pragma unroll
                 for (int v = 0; v < U; ++v) {
                     if (k0 + v >= span) break;
                     const size_t w = (size_t)item + k0 + v;
                     const unsigned y = (s_w[r + k0 + v] >> lane) & 1u;
-                    st_if(postt + w * 32 + lane, (float)a[v] * iscale, live);
-                    if (live) acc[w * 32 + lane] = Lf;
+                    float* vr = S.vrow(w, lane);
+                    st_if(vr + slot, (float)a[v] * iscale, live);
+                    if (live) reinterpret_cast<int*>(vr)[64] = Lf;
                     const unsigned neg = __ballot_sync(kFull, y ? a[v] > 0 : a[v] < 0);
                     if (lane == 0) {
                         const unsigned hw = (neg & act) | (s_old[r + k0 + v] & ~act);
@@ -551,24 +612,44 @@ __device__ __forceinline__ int sc_compact(const ScatterArgs& A, int t, int gw, i
     const int nund = ld_cg(A.ctrl + 2 * t);
     const int Gn = (nund + 31) / 32;
     const int Fb = Gn * 32;
-    const size_t slotP = (size_t)A.G * A.n * 32, slotB = (size_t)A.Gb * A.n * 32;
-    // posteriors the next check phase reads: post_1..post_{t-1} while the
-    // base is rebuilt from bits (t <= kStoreFrom), else post_{t-1}
-    for (int s = (t <= kStoreFrom ? 1 : t - 1); s <= t - 1; ++s)
-        move_lanes<float>(A.post + (s & 1) * slotP, A.post_b + (s & 1) * slotB, A.n, Gn, A.src_b, gw, nw, lane);
-    move_bits(A.noisy_w, A.noisy_b, A.n, Gn, A.src_b, gw, nw, lane);
-    move_bits(A.hard_w, A.hard_b, A.n, Gn, A.src_b, gw, nw, lane);
-    move_bits(A.syn_w, A.syn_b, A.C, Gn, A.src_b, gw, nw, lane);
-    move_bits(A.mis_w, A.mis_b, A.C, Gn, A.src_b, gw, nw, lane);
-    // acc armed with the prior (+L in the relative domain)
+    // variable blocks: the posteriors the next check phase reads (post'_1 and
+    // post'_2 while the base is rebuilt from bits, t <= kStoreFrom, else
+    // post'_{t-1}) and acc armed with the prior (+L in the relative domain)
     {
-        const long long total = (long long)Gn * A.n;
-        for (long long it = gw; it < total; it += nw) {
-            const int g2 = (int)(it / A.n), i = (int)(it - (long long)g2 * A.n);
+        const bool both = t <= kStoreFrom;
+        const int keep = ((t - 1) & 1) * 32;
+        constexpr int XU = 8;
+        const long long xchunks = (A.n + XU - 1) / XU;
+        for (long long it = gw; it < (long long)Gn * xchunks; it += nw) {
+            const int g2 = (int)(it / xchunks);
+            const int i0 = (int)(it - (long long)g2 * xchunks) * XU;
             const int s = ld_cg(A.src_b + g2 * 32 + lane);
-            A.acc_b[((size_t)g2 * A.n + i) * 32 + lane] = s >= 0 ? ld_cg(A.Lfix + s) : 0;
+            const float* src = A.vb + (s >= 0 ? ((size_t)(s >> 5) * A.n * kVB + (s & 31)) : 0);
+            float* dst = A.vb_b + (size_t)g2 * A.n * kVB + lane;
+            const int Lf = s >= 0 ? ld_cg(A.Lfix + s) : 0;
+            float v0[XU], v1[XU];
+#pragma unroll
+            for (int k = 0; k < XU; ++k) {
+                const bool ok = s >= 0 && i0 + k < A.n;
+                const size_t o = (size_t)(i0 + k) * kVB;
+                v0[k] = ok && (both || keep == 0) ? __ldca(src + o) : 0.0f;
+                v1[k] = ok && (both || keep == 32) ? __ldca(src + o + 32) : 0.0f;
+            }
+#pragma unroll
+            for (int k = 0; k < XU; ++k) {
+                if (i0 + k >= A.n) break;
+                float* d = dst + (size_t)(i0 + k) * kVB;
+                d[0] = v0[k];
+                d[32] = v1[k];
+                reinterpret_cast<int*>(d)[64] = Lf;
+            }
         }
     }
+    // (hard words are not moved: every moved frame is live in sweep t, whose
+    // variable phase writes its compacted hard word before any reader)
+    move_bits(A.noisy_w, A.noisy_b, A.n, Gn, A.src_b, gw, nw, lane);
+    move_bits(A.syn_w, A.syn_b, A.C, Gn, A.src_b, gw, nw, lane);
+    move_bits(A.mis_w, A.mis_b, A.C, Gn, A.src_b, gw, nw, lane);
     for (int s2 = gtid; s2 < Fb; s2 += nthreads) {
         const int s = ld_cg(A.src_b + s2);
         A.Lmag_b[s2] = s >= 0 ? A.Lmag[s] : 0.0f;
@@ -600,9 +681,11 @@ __device__ __forceinline__ void sc_sweep(const ScatterArgs& A, int G, int t, int
     if (t >= 2) {   // check phase
         const int total = G * A.C;
         const int ch = chunk_size(total, nwarps, CH);
-        for (int base = claim(A.work + wc, lane, ch); base < total; base = claim(A.work + wc, lane, ch))
-            sc_check_chunk<D, CPT>(A, S, base, min(base + ch, total), t, cp, lane, s_idx, s_w, s_m,
-                                   reinterpret_cast<int*>(s_x), first, scale);
+        for (int base = claim(A.work + wc, lane, ch); base < total; base = claim(A.work + wc, lane, ch)) {
+            sc_check_chunk<D, CPT>(A, S, base, min(base + ch, total), t, cp, lane,
+                                   reinterpret_cast<unsigned*>(s_idx), s_m, reinterpret_cast<int*>(s_x),
+                                   reinterpret_cast<float*>(s_v1m), first, scale);
+        }
         ++wc;
         grid_barrier(A.barrier);
         stamp(A, ts_k);
@@ -665,7 +748,7 @@ __device__ __forceinline__ void sc_sweep(const ScatterArgs& A, int G, int t, int
 }
 
 template <int D>
-__global__ void __launch_bounds__(kDecodeThreads, MBP_SCATTER_MIN_BLOCKS) decode_scatter_kernel(const ScatterArgs A)
+__global__ void __launch_bounds__(kDecodeThreads, scatter_min_blocks<D>()) decode_scatter_kernel(const ScatterArgs A)
 {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -681,16 +764,19 @@ __global__ void __launch_bounds__(kDecodeThreads, MBP_SCATTER_MIN_BLOCKS) decode
     __shared__ unsigned s_w_all[kDecodeThreads / 32][CH > 32 ? CH : 32];
     __shared__ unsigned s_x_all[kDecodeThreads / 32][CH > 32 ? CH : 32];
     __shared__ unsigned s_m_all[kDecodeThreads / 32][CH > 32 ? CH : 32];
-    // sweep-1 staging (regular column degree 6 or 9, check degree <= 16)
-    constexpr int V1 = D <= 16 ? 32 * 9 : 1;
-    __shared__ unsigned s_v1m_all[kDecodeThreads / 32][V1];
-    __shared__ uint8_t s_v1d_all[kDecodeThreads / 32][V1];
+    // per-warp scratch: sweep-1 staging (regular column degree 6 or 9, check
+    // degree <= 16: mismatch words + degrees) or, in check phases, the
+    // lane's sweep-1 magnitude per degree
+    constexpr int V1 = D <= 16 ? 32 * 9 : 0;
+    constexpr int M1T = D <= 16 ? (D + 1) * 32 : 0;
+    constexpr int RAW = (V1 + V1 / 4) > M1T ? (V1 + V1 / 4) + 1 : M1T + 1;
+    __shared__ unsigned s_raw_all[kDecodeThreads / 32][RAW];
     int* s_idx = s_idx_all[warp];
     unsigned* s_w = s_w_all[warp];
     unsigned* s_x = s_x_all[warp];
     unsigned* s_m = s_m_all[warp];
-    unsigned* s_v1m = s_v1m_all[warp];
-    uint8_t* s_v1d = s_v1d_all[warp];
+    unsigned* s_v1m = s_raw_all[warp];
+    uint8_t* s_v1d = reinterpret_cast<uint8_t*>(s_raw_all[warp] + V1);
     int* s_mf = s_idx;   // only used in the sweep-1 variable phase
 
     // fixed-point scale: |acc| <= Lmax + dv_max * clamp (+ rounding) < 2^30
@@ -793,7 +879,8 @@ __global__ void __launch_bounds__(kDecodeThreads, MBP_SCATTER_MIN_BLOCKS) decode
 // Per-frame setup: prior magnitude L = ln((1-e)/e) (init_priors,
 // decoder.py:147-152), the sweep-1 message magnitude for every degree
 // d <= Dm (the reference's sequential product of d-1 factors tanh(L/2),
-// saturation and clamp, in fp64), and the batch maximum of L.
+// saturation and clamp, in fp64), and the batch maximum of L -- all stored
+// in the kernel's log2 units (x log2 e).
 static __global__ void scatter_setup_kernel(const double* __restrict__ e, int e_stride, int B, int F, int Dm,
                                      double clamp, float* __restrict__ Lmag, float* __restrict__ Mtab,
                                      float* __restrict__ Lmax)
@@ -805,17 +892,18 @@ static __global__ void scatter_setup_kernel(const double* __restrict__ e, int e_
         const double ef = e[(long long)f * e_stride];
         L = log((1.0 - ef) / ef);
     }
-    Lmag[f] = (float)L;
+    constexpr double kLog2e = 1.4426950408889634074;
+    Lmag[f] = (float)(L * kLog2e);
     const double th = tanh(0.5 * L);
     double prod = 1.0;
     Mtab[f] = 0.0f;
     for (int d = 1; d <= Dm; ++d) {
         double r = prod >= 1.0 ? clamp : (prod <= -1.0 ? -clamp : 2.0 * atanh(prod));
         r = r > clamp ? clamp : r;
-        Mtab[(size_t)d * F + f] = f < B ? (float)r : 0.0f;
+        Mtab[(size_t)d * F + f] = f < B ? (float)(r * kLog2e) : 0.0f;
         prod *= th;
     }
-    if (f < B) atomicMax(reinterpret_cast<int*>(Lmax), __float_as_int((float)L));
+    if (f < B) atomicMax(reinterpret_cast<int*>(Lmax), __float_as_int((float)(L * kLog2e)));
 }
 
 }  // namespace mbp
