@@ -542,12 +542,19 @@ __device__ __forceinline__ void sc_var_chunk(const ScatterArgs& A, const SL<CPT>
 }
 
 // ---------------------------------------------------------------------------
-// syndrome phase (as syncheck_item); at t = 0 also stores the mismatch words
+// syndrome phase (mismatch_count, _kernels.py:310-320): 32 consecutive checks
+// of group g per warp item (lane = check); the mismatch word (bit f = frame
+// f) becomes per-frame counts via 32 ballots, returned in lane f.  At t = 0
+// the full mismatch words are stored (the sweep-1 message signs).  Callers
+// accumulate counts over their chunk and flush once per group: per-item
+// atomics on the 32 counters of a group all land on one L2 line and
+// serialise.
 // ---------------------------------------------------------------------------
-template <bool CPT>
-__device__ __forceinline__ void sc_syncheck_item(const ScatterArgs& A, const SL<CPT>& S, int g, int blk, int t,
-                                                 unsigned act, int lane)
+template <int D, bool CPT>
+__device__ __forceinline__ int sc_syncheck_item(const ScatterArgs& A, const SL<CPT>& S, int g, int blk, int t,
+                                                unsigned act, int lane)
 {
+    constexpr int DU = D < 16 ? D : 16;      // row ids loaded in parallel
     const int j = blk * 32 + lane;
     unsigned mism = 0;
     if (j < A.C) {
@@ -555,19 +562,59 @@ __device__ __forceinline__ void sc_syncheck_item(const ScatterArgs& A, const SL<
         const int d = ld_ro(A.deg + j);
         const int* row = A.chk_ell + (size_t)j * A.Ds;
         unsigned par = 0;
-        for (int k = 0; k < d; ++k) par ^= ld_cg(hw + ld_ro(row + k));
+        for (int k0 = 0; k0 < d; k0 += DU) {
+            int id[DU];
+#pragma unroll
+            for (int k = 0; k < DU; ++k) id[k] = k0 + k < d ? ld_ro(row + k0 + k) : -1;
+#pragma unroll
+            for (int k = 0; k < DU; ++k)
+                if (id[k] >= 0) par ^= ld_cg(hw + id[k]);
+        }
         const unsigned full = par ^ S.syn((size_t)g * A.C + j);
         if (t == 0) S.mis()[(size_t)g * A.C + j] = full;
         mism = full & act;
     }
     int c = 0;
+    if (__any_sync(kFull, mism != 0)) {
 #pragma unroll
-    for (int f = 0; f < 32; ++f) {
-        const int pc = __popc(__ballot_sync(kFull, (mism >> f) & 1u));
-        if (lane == f) c = pc;
+        for (int f = 0; f < 32; ++f) {
+            const int pc = __popc(__ballot_sync(kFull, (mism >> f) & 1u));
+            if (lane == f) c = pc;
+        }
+    }
+    return c;
+}
+
+// items per claim: about one claim per warp (few flushes per group line),
+// at least 8 so small batches do not spread thin
+__device__ __forceinline__ int syn_chunk(int total, int nwarps)
+{
+    return min(64, max(8, (total + nwarps - 1) / nwarps));
+}
+
+// one claimed chunk [base, end) of the syndrome phase (items g*cblk + blk)
+template <int D, bool CPT>
+__device__ __forceinline__ void sc_syncheck_chunk(const ScatterArgs& A, const SL<CPT>& S, int base, int end, int t,
+                                                  const int* cprev, int cblk, int lane)
+{
+    int g = base / cblk;
+    unsigned act = cprev ? group_mask(cprev, g, lane) : kFull;
+    int c = 0;
+    bool bad = false;
+    for (int item = base; item < end; ++item) {
+        const int gi = item / cblk;
+        if (gi != g) {
+            if (c) atomicAdd(S.cnt() + (t & 1) * S.G * 32 + g * 32 + lane, c);
+            bad |= c != 0;
+            c = 0;
+            g = gi;
+            act = cprev ? group_mask(cprev, g, lane) : kFull;
+        }
+        if (act) c += sc_syncheck_item<D, CPT>(A, S, g, item - g * cblk, t, act, lane);
     }
     if (c) atomicAdd(S.cnt() + (t & 1) * S.G * 32 + g * 32 + lane, c);
-    if (__any_sync(kFull, c != 0) && lane == 0) atomicOr(A.any_bad + (t & 1), 1);
+    bad |= c != 0;
+    if (__any_sync(kFull, bad) && lane == 0) atomicOr(A.any_bad + (t & 1), 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -732,17 +779,9 @@ __device__ __forceinline__ void sc_sweep(const ScatterArgs& A, int G, int t, int
     stamp(A, ts_k);
     {   // syndrome phase
         const int total = G * cblk;
-        for (int base = claim(A.work + wc, lane, kSynChunk); base < total;
-             base = claim(A.work + wc, lane, kSynChunk)) {
-            const int end = min(base + kSynChunk, total);
-            int g = base / cblk;
-            unsigned act = group_mask(cp, g, lane);
-            for (int item = base; item < end; ++item) {
-                const int gi = item / cblk;
-                if (gi != g) { g = gi; act = group_mask(cp, g, lane); }
-                if (act) sc_syncheck_item<CPT>(A, S, g, item - g * cblk, t, act, lane);
-            }
-        }
+        const int sc = syn_chunk(total, nwarps);
+        for (int base = claim(A.work + wc, lane, sc); base < total; base = claim(A.work + wc, lane, sc))
+            sc_syncheck_chunk<D, CPT>(A, S, base, min(base + sc, total), t, cp, cblk, lane);
         ++wc;
     }
 }
@@ -804,10 +843,9 @@ __global__ void __launch_bounds__(kDecodeThreads, scatter_min_blocks<D>()) decod
     {
         const SL<false> S0{A, A.G};
         const int total = A.G * cblk;
-        for (int base = claim(A.work + wc, lane, kSynChunk); base < total;
-             base = claim(A.work + wc, lane, kSynChunk))
-            for (int item = base; item < min(base + kSynChunk, total); ++item)
-                sc_syncheck_item<false>(A, S0, item / cblk, item % cblk, 0, kFull, lane);
+        const int sc = syn_chunk(total, nwarps);
+        for (int base = claim(A.work + wc, lane, sc); base < total; base = claim(A.work + wc, lane, sc))
+            sc_syncheck_chunk<D, false>(A, S0, base, min(base + sc, total), 0, nullptr, cblk, lane);
         ++wc;
     }
 
