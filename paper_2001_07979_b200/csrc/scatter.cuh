@@ -224,13 +224,15 @@ __device__ __forceinline__ void rule_sd(const float (&x)[DD], int d, unsigned fl
 // first gather (post'_{s0-1}) of the next row is issued before the current
 // row's rule (software pipeline).  FULL: every lane of the group is live.
 // ---------------------------------------------------------------------------
-template <int D, int DD, bool PAD, bool FULL, bool SAT, bool CPT>
+template <int D, int DD, bool PAD, bool FULL, bool SAT, bool T2, bool CPT>
 __device__ __forceinline__ void sc_row(const ScatterArgs& A, const SL<CPT>& S, const float (&p)[D], int d,
-                                       unsigned sj, float M1, const unsigned* soff, bool live, int t,
-                                       const float* gb, const float* qrow, float* crow, float scale)
+                                       unsigned sj, float M1, const unsigned* soff, bool live, int t_,
+                                       const float* gb, const float* qrow, float* crow, float scale, bool absolute)
 {
+    // T2: sweep 2, the hot case (no chain, no store) compiled on its own
+    const int t = T2 ? 2 : t_;
     const bool lv = FULL || live;
-    const bool explicit_base = t > kStoreFrom;
+    const bool explicit_base = !T2 && t > kStoreFrom;
     float c[DD];
     if (!explicit_base) {
         const float c1 = sj ? -M1 : M1;          // c2v'_1, the same on every edge of the row
@@ -243,15 +245,30 @@ __device__ __forceinline__ void sc_row(const ScatterArgs& A, const SL<CPT>& S, c
     float x[DD];
 #pragma unroll
     for (int k = 0; k < DD; ++k) x[k] = p[k] - c[k];
-    rule_sd<DD, PAD, SAT>(x, d, sj, A.clamp, A.sat, c);
-    for (int s = (explicit_base ? t : 2) + 1; s <= t; ++s) {
-        const float* gs = gb + ((s - 1) & 1) * 32;   // post'_{s-1} line
+    // acc holds prior + sum of c2v'_{t-1} (fixed point); adding the rounded
+    // differences c2v'_t - c2v'_{t-1} leaves prior + sum of c2v'_t exactly
+    int vold[DD];
+    if (t == 2) {
+        const int v1 = __float2int_rn(c[0] * scale);   // row constant
 #pragma unroll
-        for (int k = 0; k < DD; ++k) {
-            const float* q = byte_off(gs, soff[k]);
-            x[k] = (FULL ? ld_cg(q) : ld_cg_if(q, live)) - c[k];
+        for (int k = 0; k < DD; ++k) vold[k] = v1;
+    } else if (explicit_base) {
+#pragma unroll
+        for (int k = 0; k < DD; ++k) vold[k] = __float2int_rn(c[k] * scale);
+    }
+    rule_sd<DD, PAD, SAT>(x, d, sj, A.clamp, A.sat, c);
+    if (t > 2 && !explicit_base) {
+        // chain: c2v'_s from post'_{s-1}, s = 3 .. t (vold = c2v'_{t-1})
+        for (int s = 3; s <= t; ++s) {
+            const float* gs = gb + ((s - 1) & 1) * 32;   // post'_{s-1} line
+#pragma unroll
+            for (int k = 0; k < DD; ++k) {
+                const float* q = byte_off(gs, soff[k]);
+                x[k] = (FULL ? ld_cg(q) : ld_cg_if(q, live)) - c[k];
+                if (s == t) vold[k] = __float2int_rn(c[k] * scale);
+            }
+            rule_sd<DD, PAD, SAT>(x, d, sj, A.clamp, A.sat, c);
         }
-        rule_sd<DD, PAD, SAT>(x, d, sj, A.clamp, A.sat, c);
     }
     if (t >= kStoreFrom) {
         // padded-ELL rows own Ds slots, so pad slots may be written
@@ -260,7 +277,7 @@ __device__ __forceinline__ void sc_row(const ScatterArgs& A, const SL<CPT>& S, c
     }
 #pragma unroll
     for (int k = 0; k < DD; ++k) {
-        const int v = __float2int_rn(c[k] * scale);
+        const int v = __float2int_rn(c[k] * scale) - (CPT && absolute ? 0 : vold[k]);
         red_add(byte_off(gb, soff[k]) + 64, (lv && (!PAD || k < d)) ? v : 0);   // acc line
     }
 }
@@ -280,14 +297,15 @@ __device__ __forceinline__ const float* sc_c2v_in_base(const ScatterArgs& A, con
 }
 
 // rows [r0, r1) of the staged chunk, all in group g (first row j0)
-template <int D, bool FULL, bool SAT, bool CPT>
+template <int D, bool FULL, bool SAT, bool T2, bool CPT>
 __device__ __forceinline__ void sc_span(const ScatterArgs& A, const SL<CPT>& S, int g, int j0, int r0, int r1, int t,
                                         unsigned act, int lane, const unsigned* s_off, const unsigned* s_m,
                                         const int* s_d, const float* s_m1, bool first, float scale)
 {
     constexpr int SD = Chunk<D>::SD;
+    if (T2) t = 2;
     const bool live = (act >> lane) & 1u;
-    const bool explicit_base = t > kStoreFrom;
+    const bool explicit_base = !T2 && t > kStoreFrom;
     const float* gb = S.vrow((size_t)g * A.n, lane);
     const float* qb = explicit_base ? sc_c2v_in_base<CPT>(A, S, g, lane, first) : nullptr;
     // first gather: post'_{s0-1}
@@ -323,12 +341,12 @@ __device__ __forceinline__ void sc_span(const ScatterArgs& A, const SL<CPT>& S, 
         const float* qrow = explicit_base ? qb + (size_t)j * A.Ds * 32 : nullptr;
         float* crow = t >= kStoreFrom ? S.c2v() + ((size_t)g * A.slots + (size_t)j * A.Ds) * 32 + lane : nullptr;
         if (d == D)
-            sc_row<D, D, false, FULL, SAT, CPT>(A, S, p, d, sj, M1, soff, live, t, gb, qrow, crow, scale);
+            sc_row<D, D, false, FULL, SAT, T2, CPT>(A, S, p, d, sj, M1, soff, live, t, gb, qrow, crow, scale, first);
         else if (D > 1 && d == D - 1)
-            sc_row<D, (D > 1 ? D - 1 : 1), false, FULL, SAT, CPT>(A, S, p, d, sj, M1, soff, live, t, gb, qrow,
-                                                                  crow, scale);
+            sc_row<D, (D > 1 ? D - 1 : 1), false, FULL, SAT, T2, CPT>(A, S, p, d, sj, M1, soff, live, t, gb, qrow,
+                                                                      crow, scale, first);
         else
-            sc_row<D, D, true, FULL, SAT, CPT>(A, S, p, d, sj, M1, soff, live, t, gb, qrow, crow, scale);
+            sc_row<D, D, true, FULL, SAT, T2, CPT>(A, S, p, d, sj, M1, soff, live, t, gb, qrow, crow, scale, first);
     }
 }
 
@@ -365,13 +383,19 @@ __device__ __forceinline__ void sc_check_chunk(const ScatterArgs& A, const SL<CP
                     __syncwarp();
                 }
             }
-            // fast variant: every lane live and no input can saturate
-            if (act == kFull && A.clamp < A.sat)
-                sc_span<D, true, false, CPT>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d, s_m1, first,
-                                             scale);
-            else
-                sc_span<D, false, true, CPT>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d, s_m1, first,
-                                             scale);
+            // fast variants: every lane live and no input can saturate, sweep
+            // 2 (the hot case) compiled on its own
+            if (act == kFull && A.clamp < A.sat) {
+                if (t == 2)
+                    sc_span<D, true, false, true, CPT>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d, s_m1,
+                                                       first, scale);
+                else
+                    sc_span<D, true, false, false, CPT>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d,
+                                                        s_m1, first, scale);
+            } else {
+                sc_span<D, false, true, false, CPT>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d, s_m1,
+                                                    first, scale);
+            }
             __syncwarp();
         }
         r += span;
@@ -416,7 +440,7 @@ __device__ __forceinline__ void sc_var1_item(const ScatterArgs& A, const SL<CPT>
     }
     float* vr = S.vrow(w, lane);
     st_if(vr + 32, (float)a * iscale, live);
-    if (live) reinterpret_cast<int*>(vr)[64] = Lf;
+    if (live) reinterpret_cast<int*>(vr)[64] = a;   // acc = post'_1 in fixed point
     const unsigned neg = __ballot_sync(kFull, y ? a > 0 : a < 0);
     if (lane == 0) {
         // the iteration-0 decision of every frame is its noisy key
@@ -433,24 +457,31 @@ __device__ __forceinline__ void sc_var1_item(const ScatterArgs& A, const SL<CPT>
 template <int D, int DV, bool CPT>
 __device__ __forceinline__ void sc_var1_chunk(const ScatterArgs& A, const SL<CPT>& S, int base, int end,
                                               const int* cprev, int lane, unsigned* s_mis, uint8_t* s_deg,
-                                              int* s_mf, float iscale)
+                                              unsigned* s_y, int* s_mf, float iscale)
 {
     const int rows = end - base;
     const int tot = rows * DV;
-#pragma unroll 4
-    for (int idx = lane; idx < tot; idx += 32) {
-        const int v = idx / DV, k = idx - v * DV;
-        const int item = base + v;
-        const int g = item / A.n, i = item - g * A.n;
-        const int j = ld_ro(A.var_chk + (size_t)i * DV + k);
-        s_mis[idx] = ld_cg(S.mis() + (size_t)g * A.C + j);
-        s_deg[idx] = ld_ro(A.deg + j);
+    // lane v: group / variable of chunk row v (one division per lane)
+    const int gl_ = (base + lane) / A.n;
+    const int il_ = base + lane - gl_ * A.n;
+    if (lane < rows) s_y[lane] = S.noisy(base + lane);
+    for (int b0 = 0; b0 < tot; b0 += 32) {
+        const int idx = b0 + lane;
+        const int v = idx < tot ? idx / DV : 0;
+        const int k = idx - v * DV;
+        const int gv = __shfl_sync(kFull, gl_, v);
+        const int iv = __shfl_sync(kFull, il_, v);
+        if (idx < tot) {
+            const int j = ld_ro(A.var_chk + (size_t)iv * DV + k);
+            s_mis[idx] = ld_cg(S.mis() + (size_t)gv * A.C + j);
+            s_deg[idx] = ld_ro(A.deg + j);
+        }
     }
     __syncwarp();
     int r = 0;
     while (r < rows) {
         const int item = base + r;
-        const int g = item / A.n;
+        const int g = __shfl_sync(kFull, gl_, r);
         const int i = item - g * A.n;
         const int span = min(rows - r, A.n - i);
         const unsigned act = group_mask(cprev, g, lane);
@@ -462,7 +493,7 @@ __device__ __forceinline__ void sc_var1_chunk(const ScatterArgs& A, const SL<CPT
             const int Lf = S.Lfix(g * 32 + lane);
             for (int v = r; v < r + span; ++v) {
                 const size_t w = (size_t)base + v;
-                const unsigned yw = S.noisy(w);
+                const unsigned yw = s_y[v];
                 const unsigned y = (yw >> lane) & 1u;
                 int a = Lf;
 #pragma unroll
@@ -473,7 +504,7 @@ __device__ __forceinline__ void sc_var1_chunk(const ScatterArgs& A, const SL<CPT
                 }
                 float* vr = S.vrow(w, lane);
                 st_if(vr + 32, (float)a * iscale, live);
-                if (live) reinterpret_cast<int*>(vr)[64] = Lf;
+                if (live) reinterpret_cast<int*>(vr)[64] = a;   // acc = post'_1 in fixed point
                 const unsigned neg = __ballot_sync(kFull, y ? a > 0 : a < 0);
                 if (lane == 0) {
                     const unsigned hw = (neg & act) | (yw & ~act);
@@ -488,7 +519,8 @@ __device__ __forceinline__ void sc_var1_chunk(const ScatterArgs& A, const SL<CPT
     __syncwarp();
 }
 
-// sweep t >= 2: acc -> post'_t, hard decision, re-arm acc with the prior.
+// sweep t >= 2: acc -> post'_t and the hard decision (acc is not re-armed:
+// the check phase adds message differences).
 template <bool CPT>
 __device__ __forceinline__ void sc_var_chunk(const ScatterArgs& A, const SL<CPT>& S, int base, int end, int t,
                                              const int* cprev, int lane, unsigned* s_w, unsigned* s_old,
@@ -510,8 +542,7 @@ __device__ __forceinline__ void sc_var_chunk(const ScatterArgs& A, const SL<CPT>
         const unsigned act = group_mask(cprev, g, lane);
         if (act) {
             const bool live = (act >> lane) & 1u;
-            const int Lf = S.Lfix(g * 32 + lane);
-            constexpr int U = 4;   // independent acc loads in flight
+            constexpr int U = 8;   // independent acc loads in flight
             for (int k0 = 0; k0 < span; k0 += U) {
                 int a[U];
 #pragma unroll
@@ -526,7 +557,6 @@ __device__ __forceinline__ void sc_var_chunk(const ScatterArgs& A, const SL<CPT>
                     const unsigned y = (s_w[r + k0 + v] >> lane) & 1u;
                     float* vr = S.vrow(w, lane);
                     st_if(vr + slot, (float)a[v] * iscale, live);
-                    if (live) reinterpret_cast<int*>(vr)[64] = Lf;
                     const unsigned neg = __ballot_sync(kFull, y ? a[v] > 0 : a[v] < 0);
                     if (lane == 0) {
                         const unsigned hw = (neg & act) | (s_old[r + k0 + v] & ~act);
@@ -661,7 +691,8 @@ __device__ __forceinline__ int sc_compact(const ScatterArgs& A, int t, int gw, i
     const int Fb = Gn * 32;
     // variable blocks: the posteriors the next check phase reads (post'_1 and
     // post'_2 while the base is rebuilt from bits, t <= kStoreFrom, else
-    // post'_{t-1}) and acc armed with the prior (+L in the relative domain)
+    // post'_{t-1}); acc is re-armed with the prior (+L in the relative
+    // domain) and the first compacted check phase adds absolute messages
     {
         const bool both = t <= kStoreFrom;
         const int keep = ((t - 1) & 1) * 32;
@@ -747,11 +778,11 @@ __device__ __forceinline__ void sc_sweep(const ScatterArgs& A, int G, int t, int
                 const int ch = chunk_size(total, nwarps, 32);
                 for (int base = claim(A.work + wc, lane, ch); base < total; base = claim(A.work + wc, lane, ch)) {
                     if (A.dv_max == 6)
-                        sc_var1_chunk<D, 6, CPT>(A, S, base, min(base + ch, total), cp, lane, s_v1m, s_v1d, s_mf,
-                                                 iscale);
+                        sc_var1_chunk<D, 6, CPT>(A, S, base, min(base + ch, total), cp, lane, s_v1m, s_v1d, s_w,
+                                                 s_mf, iscale);
                     else
-                        sc_var1_chunk<D, 9, CPT>(A, S, base, min(base + ch, total), cp, lane, s_v1m, s_v1d, s_mf,
-                                                 iscale);
+                        sc_var1_chunk<D, 9, CPT>(A, S, base, min(base + ch, total), cp, lane, s_v1m, s_v1d, s_w,
+                                                 s_mf, iscale);
                 }
             }
         } else if (t == 1) {
