@@ -28,7 +28,8 @@ LIB = LIB_DIR / "libmbp_b200.so"
 UNITS = [
     ("mbp", "mbp.cu", []),
     ("k_explicit_f32", "k_explicit.cu", []),
-    ("k_explicit_f64", "k_explicit.cu", ["-DMBP_EXPLICIT_F64"]),
+    ("k_explicit_f64", "k_explicit.cu", ["-DMBP_EXPLICIT_F64=1"]),
+    ("k_explicit_f64w", "k_explicit.cu", ["-DMBP_EXPLICIT_F64=2"]),
     ("k_scatter_0", "k_scatter.cu", ["-DMBP_SCATTER_PART=0"]),
     ("k_scatter_1", "k_scatter.cu", ["-DMBP_SCATTER_PART=1"]),
     ("k_scatter_2", "k_scatter.cu", ["-DMBP_SCATTER_PART=2"]),
@@ -53,16 +54,22 @@ def stale() -> bool:
     return any(p.stat().st_mtime > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) -> Path:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False, defines=(),
+          out: Path | None = None) -> Path:
+    """Compile the units in parallel and link; ``defines``/``out`` build a
+    variant library elsewhere (experiments, e.g. MBP_SCATTER_MIN_BLOCKS=3)."""
+    lib = Path(out) if out else LIB
+    obj_dir = lib.parent / "obj"
+    if not force and not out and not stale():
         return LIB
-    OBJ_DIR.mkdir(parents=True, exist_ok=True)
+    obj_dir.mkdir(parents=True, exist_ok=True)
     cc = nvcc()
 
     def compile_unit(unit):
         name, src, defs = unit
-        obj = OBJ_DIR / f"{name}.o"
-        cmd = [cc, *NVCC_FLAGS, *defs, *(["-Xptxas", "-v"] if ptxas_info else []), "-c", "-o", str(obj),
+        obj = obj_dir / f"{name}.o"
+        cmd = [cc, *NVCC_FLAGS, *defs, *[f"-D{d}" for d in defines], *(["-Xptxas", "-v"] if ptxas_info else []),
+               "-c", "-o", str(obj),
                str(CSRC / src)]
         if verbose:
             print(" ".join(cmd), flush=True)
@@ -75,14 +82,22 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) 
 
     with ThreadPoolExecutor(max_workers=len(UNITS)) as pool:
         objs = list(pool.map(compile_unit, UNITS))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
-    tmp.replace(LIB)
-    return LIB
+    tmp.replace(lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True, ptxas_info="--ptxas" in sys.argv))
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--ptxas", action="store_true")
+    ap.add_argument("-D", dest="defines", action="append", default=[])
+    ap.add_argument("--out")
+    a = ap.parse_args()
+    print(build(force=a.force, verbose=True, ptxas_info=a.ptxas, defines=a.defines, out=a.out))

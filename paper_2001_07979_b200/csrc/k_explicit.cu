@@ -26,10 +26,25 @@ static cudaError_t dispatch(const DecodeArgs<Real>& A, int D, bool damp, bool is
     }
 }
 
-#ifdef MBP_EXPLICIT_F64
+// fp64 instances are split over two objects (MBP_EXPLICIT_F64 = 1: D <= 16,
+// 2: D >= 32) so the slowest unit of the parallel build halves
+#if defined(MBP_EXPLICIT_F64) && MBP_EXPLICIT_F64 == 1
 cudaError_t launch_explicit_f64(const DecodeArgs<double>& A, int D, bool damp, bool iso, int sm, cudaStream_t s)
 {
-    return dispatch<double>(A, D, damp, iso, sm, s);
+    switch (D) {
+    case 8: return variant<double, 8>(A, damp, iso, sm, s);
+    case 16: return variant<double, 16>(A, damp, iso, sm, s);
+    default: return launch_explicit_f64_wide(A, D, damp, iso, sm, s);
+    }
+}
+#elif defined(MBP_EXPLICIT_F64) && MBP_EXPLICIT_F64 == 2
+cudaError_t launch_explicit_f64_wide(const DecodeArgs<double>& A, int D, bool damp, bool iso, int sm, cudaStream_t s)
+{
+    switch (D) {
+    case 32: return variant<double, 32>(A, damp, iso, sm, s);
+    case 64: return variant<double, 64>(A, damp, iso, sm, s);
+    default: return cudaErrorNotSupported;
+    }
 }
 #else
 cudaError_t launch_explicit_f32(const DecodeArgs<float>& A, int D, bool damp, bool iso, int sm, cudaStream_t s)

@@ -14,6 +14,8 @@ cudaError_t launch_explicit_f32(const DecodeArgs<float>& A, int D, bool damp, bo
                                 cudaStream_t s);
 cudaError_t launch_explicit_f64(const DecodeArgs<double>& A, int D, bool damp, bool iso, int sm_count,
                                 cudaStream_t s);
+cudaError_t launch_explicit_f64_wide(const DecodeArgs<double>& A, int D, bool damp, bool iso, int sm_count,
+                                     cudaStream_t s);   // D >= 32
 cudaError_t launch_scatter_small(const ScatterArgs& A, int D, int sm_count, cudaStream_t s);   // D 3..8
 cudaError_t launch_scatter_mid(const ScatterArgs& A, int D, int sm_count, cudaStream_t s);     // D 9..16
 cudaError_t launch_scatter_large(const ScatterArgs& A, int D, int sm_count, cudaStream_t s);   // D 20..64

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -112,6 +113,9 @@ struct mbp_workspace {
     int ts_cap = 0;
     int Gb = 0;        // compaction capacity (groups), 0 = disabled
     cudaStream_t own_stream = nullptr;
+    cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;   // host-path pipeline
+    static constexpr int kMaxSub = 8;
+    cudaEvent_t ev_in[kMaxSub] = {}, ev_out[kMaxSub] = {}, ev_d2h = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
     int last_B = 0;
     bool timed = false, e2e_timed = false;
@@ -121,7 +125,14 @@ struct mbp_workspace {
         if (ev1) cudaEventDestroy(ev1);
         if (ev2) cudaEventDestroy(ev2);
         if (ev3) cudaEventDestroy(ev3);
+        for (int i = 0; i < kMaxSub; ++i) {
+            if (ev_in[i]) cudaEventDestroy(ev_in[i]);
+            if (ev_out[i]) cudaEventDestroy(ev_out[i]);
+        }
+        if (ev_d2h) cudaEventDestroy(ev_d2h);
         if (own_stream) cudaStreamDestroy(own_stream);
+        if (h2d_stream) cudaStreamDestroy(h2d_stream);
+        if (d2h_stream) cudaStreamDestroy(d2h_stream);
     }
 };
 
@@ -371,7 +382,13 @@ int mbp_workspace_create(mbp_ensemble* ens, int32_t max_frames, const mbp_decode
     ws->G = (max_frames + 31) / 32;
     ws->real_size = cfg->precision == MBP_FP64_TANH ? 8 : 4;
     if ((rc = ws_alloc(ws))) { delete ws; return rc; }
-    if (cudaStreamCreateWithFlags(&ws->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+    bool ok = cudaStreamCreateWithFlags(&ws->h2d_stream, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&ws->d2h_stream, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ws->ev_d2h, cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; ok && i < mbp_workspace::kMaxSub; ++i)
+        ok = cudaEventCreateWithFlags(&ws->ev_in[i], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&ws->ev_out[i], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok || cudaStreamCreateWithFlags(&ws->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreate(&ws->ev0) != cudaSuccess || cudaEventCreate(&ws->ev1) != cudaSuccess ||
         cudaEventCreate(&ws->ev2) != cudaSuccess || cudaEventCreate(&ws->ev3) != cudaSuccess) {
         delete ws;
@@ -689,6 +706,23 @@ static int ensure(DevBuf& b, size_t bytes)
     return b.bytes >= bytes ? MBP_OK : b.alloc(bytes);
 }
 
+// Host-buffer path.  The batch is split into sub-batches whose H2D copies
+// (h2d_stream) and D2H copies (d2h_stream) overlap the decode of their
+// neighbours on the workspace stream -- the decode kernel owns every SM, the
+// copies only the copy engines.  The diagnostic modes (kept state, decision
+// history, phase stamps) read the last decode's buffers, so they decode the
+// batch as one piece.
+static int host_subbatches(const mbp_workspace* ws, int64_t batch)
+{
+    if (ws->cfg.flags & (MBP_KEEP_STATE | MBP_RECORD_HISTORY | MBP_PROFILE_PHASES)) return 1;
+    if (batch > ws->cap) return 1;   // the device path already works in cap-sized chunks
+    // the decode kernel's efficiency falls below ~1024 frames per launch
+    // (fixed per-sweep costs), so only large host batches are split
+    if (const char* v = std::getenv("MBP_HOST_SUBBATCHES"))
+        return (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)std::atoi(v), mbp_workspace::kMaxSub, batch / 32}));
+    return (int)std::max<int64_t>(1, std::min<int64_t>(mbp_workspace::kMaxSub, batch / 1024));
+}
+
 int mbp_decode_batch(mbp_workspace* ws, const uint8_t* noisy, const uint8_t* syn, const double* e,
                      int32_t e_stride, int64_t batch, uint8_t* corrected, uint8_t* converged,
                      int32_t* iterations, int32_t* mismatches)
@@ -709,18 +743,44 @@ int mbp_decode_batch(mbp_workspace* ws, const uint8_t* noisy, const uint8_t* syn
         return rc;
     uint8_t* d_noisy = ws->tmp_in.as<uint8_t>();
     uint8_t* d_syn = d_noisy + batch * nb;
+    const int nsub = host_subbatches(ws, batch);
+    // sub-batch k = frames [off[k], off[k+1]), offsets multiples of 32
+    int64_t off[mbp_workspace::kMaxSub + 1];
+    const int64_t per = ((batch + nsub - 1) / nsub + 31) / 32 * 32;
+    for (int k = 0; k <= nsub; ++k) off[k] = std::min<int64_t>(batch, per * k);
     MBP_CUDA(cudaEventRecord(ws->ev2, s));
-    MBP_CUDA(cudaMemcpyAsync(d_noisy, noisy, batch * nb, cudaMemcpyHostToDevice, s));
-    MBP_CUDA(cudaMemcpyAsync(d_syn, syn, batch * sb, cudaMemcpyHostToDevice, s));
-    MBP_CUDA(cudaMemcpyAsync(ws->tmp_e.p, e, ne * 8, cudaMemcpyHostToDevice, s));
-    if ((rc = mbp_decode_batch_device(ws, d_noisy, d_syn, ws->tmp_e.as<double>(), e_stride, batch,
-                                      ws->tmp_out.as<uint8_t>(), ws->tmp_conv.as<uint8_t>(),
-                                      ws->tmp_iters.as<int>(), ws->tmp_mism.as<int>(), s)))
-        return rc;
-    MBP_CUDA(cudaMemcpyAsync(corrected, ws->tmp_out.p, batch * nb, cudaMemcpyDeviceToHost, s));
-    MBP_CUDA(cudaMemcpyAsync(converged, ws->tmp_conv.p, batch, cudaMemcpyDeviceToHost, s));
-    MBP_CUDA(cudaMemcpyAsync(iterations, ws->tmp_iters.p, batch * 4, cudaMemcpyDeviceToHost, s));
-    MBP_CUDA(cudaMemcpyAsync(mismatches, ws->tmp_mism.p, batch * 4, cudaMemcpyDeviceToHost, s));
+    MBP_CUDA(cudaStreamWaitEvent(ws->h2d_stream, ws->ev2, 0));
+    MBP_CUDA(cudaStreamWaitEvent(ws->d2h_stream, ws->ev2, 0));
+    MBP_CUDA(cudaMemcpyAsync(ws->tmp_e.p, e, ne * 8, cudaMemcpyHostToDevice, ws->h2d_stream));
+    for (int k = 0; k < nsub; ++k) {
+        const int64_t a = off[k], n = off[k + 1] - off[k];
+        if (n <= 0) continue;
+        MBP_CUDA(cudaMemcpyAsync(d_noisy + a * nb, noisy + a * nb, n * nb, cudaMemcpyHostToDevice, ws->h2d_stream));
+        MBP_CUDA(cudaMemcpyAsync(d_syn + a * sb, syn + a * sb, n * sb, cudaMemcpyHostToDevice, ws->h2d_stream));
+        MBP_CUDA(cudaEventRecord(ws->ev_in[k], ws->h2d_stream));
+    }
+    for (int k = 0; k < nsub; ++k) {
+        const int64_t a = off[k], n = off[k + 1] - off[k];
+        if (n <= 0) continue;
+        MBP_CUDA(cudaStreamWaitEvent(s, ws->ev_in[k], 0));
+        if ((rc = mbp_decode_batch_device(ws, d_noisy + a * nb, d_syn + a * sb,
+                                          ws->tmp_e.as<double>() + (e_stride ? a : 0), e_stride, n,
+                                          ws->tmp_out.as<uint8_t>() + a * nb, ws->tmp_conv.as<uint8_t>() + a,
+                                          ws->tmp_iters.as<int>() + a, ws->tmp_mism.as<int>() + a, s)))
+            return rc;
+        MBP_CUDA(cudaEventRecord(ws->ev_out[k], s));
+        MBP_CUDA(cudaStreamWaitEvent(ws->d2h_stream, ws->ev_out[k], 0));
+        MBP_CUDA(cudaMemcpyAsync(corrected + a * nb, ws->tmp_out.as<uint8_t>() + a * nb, n * nb,
+                                 cudaMemcpyDeviceToHost, ws->d2h_stream));
+        MBP_CUDA(cudaMemcpyAsync(converged + a, ws->tmp_conv.as<uint8_t>() + a, n, cudaMemcpyDeviceToHost,
+                                 ws->d2h_stream));
+        MBP_CUDA(cudaMemcpyAsync(iterations + a, ws->tmp_iters.as<int>() + a, n * 4, cudaMemcpyDeviceToHost,
+                                 ws->d2h_stream));
+        MBP_CUDA(cudaMemcpyAsync(mismatches + a, ws->tmp_mism.as<int>() + a, n * 4, cudaMemcpyDeviceToHost,
+                                 ws->d2h_stream));
+    }
+    MBP_CUDA(cudaEventRecord(ws->ev_d2h, ws->d2h_stream));
+    MBP_CUDA(cudaStreamWaitEvent(s, ws->ev_d2h, 0));
     MBP_CUDA(cudaEventRecord(ws->ev3, s));
     MBP_CUDA(cudaStreamSynchronize(s));
     ws->e2e_timed = true;

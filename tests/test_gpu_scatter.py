@@ -1,0 +1,159 @@
+"""Parity of the production scatter decode kernel (csrc/scatter.cuh) with the
+oracle (the reference's decode_loop restated in C) on configurations the
+golden fixtures do not cover: per-frame crossover probabilities (a sweep-1
+message table per frame), a clamp above the fp64 tanh saturation point (the
+SAT code path), the explicit-message base of sweeps >= 4 with and without
+frame compaction, the wide-row (degree 13/14, 128-register) instances, the
+pipelined host path, and equality with the explicit-message kernel.
+
+Bar: per frame `converged`, `iterations_used`,
+`residual_syndrome_mismatches` equal to the oracle, corrected bits of
+converged frames equal; posteriors within |d| <= 1e-4 * max(|ref|, 1).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2001_07979_b200 import BatchDecoder, DecoderConfig
+from paper_2001_07979_b200 import _native as N
+from paper_2001_07979_b200.bits import unpack_rows
+from paper_2001_07979_b200.channel import make_frames
+from paper_2001_07979_b200.matrix import stacked_layout
+
+pytestmark = pytest.mark.gpu
+
+
+def _syn_bits(rows, u, m):
+    mb = (m + 7) // 8
+    return np.concatenate([unpack_rows(rows[:, l * mb:(l + 1) * mb], m) for l in range(u)], axis=1)
+
+
+def _oracle_all(ens, noisy, syn, e, cfg, frames=None):
+    lay = stacked_layout(ens)
+    og = oracle.OracleGraph(lay)
+    nb = unpack_rows(noisy, ens.n)
+    sb = _syn_bits(syn, ens.u, ens.m)
+    ev = np.broadcast_to(np.asarray(e, dtype=np.float64), (noisy.shape[0],))
+    out = []
+    for k in (range(noisy.shape[0]) if frames is None else frames):
+        out.append(oracle.decode(og, nb[k], sb[k], float(ev[k]), max_iterations=cfg.max_iterations,
+                                 clamp=cfg.llr_clamp, damping=cfg.damping,
+                                 joint=cfg.combining_mode == "joint-graph"))
+    return out
+
+
+def _assert_matches(res, ref, frames=None):
+    idx = list(range(len(ref))) if frames is None else list(frames)
+    for r, k in zip(ref, idx):
+        assert bool(res.converged[k]) == r["converged"], k
+        assert int(res.iterations[k]) == r["iterations"], k
+        assert int(res.mismatches[k]) == r["mismatches"], k
+        if r["converged"]:
+            assert np.array_equal(res.corrected[k], np.packbits(r["hard"], bitorder="little")), k
+
+
+def test_per_frame_crossover_probabilities(cfg1_ensemble):
+    """One e per frame: the prior and the sweep-1 message magnitudes differ
+    per lane (decode with frames drawn at 3-9 % but decoded with their own e)."""
+    rng = np.random.default_rng(21)
+    B = 96
+    es = rng.uniform(0.03, 0.09, size=B)
+    fb = [make_frames(cfg1_ensemble.n, float(es[k]), 1, seed=100 + k) for k in range(B)]
+    keys = np.concatenate([f.keys for f in fb])
+    noisy = np.concatenate([f.noisy for f in fb])
+    dec = BatchDecoder(cfg1_ensemble, B)
+    syn = dec.syndromes(keys)
+    res = dec.decode(noisy, syn, es)
+    _assert_matches(res, _oracle_all(cfg1_ensemble, noisy, syn, es, DecoderConfig()))
+
+
+@pytest.mark.parametrize("clamp", [40.0, 60.0])
+def test_clamp_above_saturation(cfg1_ensemble, clamp):
+    """llr_clamp >= the fp64 tanh saturation point (~38.1): inputs with
+    |x| >= sat must act as t = 1 exactly (the SAT path of rule_sd)."""
+    cfg = DecoderConfig(llr_clamp=clamp)
+    fb = make_frames(cfg1_ensemble.n, 0.08, 64, seed=31)
+    dec = BatchDecoder(cfg1_ensemble, 64, cfg)
+    syn = dec.syndromes(fb.keys)
+    res = dec.decode(fb.noisy, syn, 0.08)
+    _assert_matches(res, _oracle_all(cfg1_ensemble, fb.noisy, syn, 0.08, cfg))
+
+
+@pytest.mark.parametrize("compaction", [True, False])
+def test_long_decodes_explicit_base(cfg1_ensemble, compaction):
+    """e = 0.10 at R = 1/2, n = 4096: many frames need 4..60 sweeps (explicit
+    c2v base from sweep 4), some fail; with and without compaction."""
+    flags = 0 if compaction else N.MBP_NO_COMPACTION
+    fb = make_frames(cfg1_ensemble.n, 0.10, 160, seed=41)
+    dec = BatchDecoder(cfg1_ensemble, 160, flags=flags)
+    syn = dec.syndromes(fb.keys)
+    res = dec.decode(fb.noisy, syn, 0.10)
+    assert res.iterations.max() >= 5
+    _assert_matches(res, _oracle_all(cfg1_ensemble, fb.noisy, syn, 0.10, DecoderConfig()))
+
+
+def test_scatter_equals_explicit_kernel(cfg1_ensemble):
+    """Same decisions from the scatter kernel and the explicit-message kernel
+    (both fp32); posteriors within the fp32 tolerance of each other."""
+    fb = make_frames(cfg1_ensemble.n, 0.07, 64, seed=51)
+    sc = BatchDecoder(cfg1_ensemble, 64)
+    ex = BatchDecoder(cfg1_ensemble, 64, flags=N.MBP_EXPLICIT_MESSAGES)
+    syn = sc.syndromes(fb.keys)
+    a = sc.decode(fb.noisy, syn, 0.07)
+    b = ex.decode(fb.noisy, syn, 0.07)
+    for f in ("corrected", "converged", "iterations", "mismatches"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
+    for t in (1, 2, 3):
+        cfg = DecoderConfig(max_iterations=t)
+        s2 = BatchDecoder(cfg1_ensemble, 64, cfg, flags=N.MBP_KEEP_STATE)
+        e2 = BatchDecoder(cfg1_ensemble, 64, cfg, flags=N.MBP_KEEP_STATE | N.MBP_EXPLICIT_MESSAGES)
+        s2.decode(fb.noisy, syn, 0.07)
+        e2.decode(fb.noisy, syn, 0.07)
+        for k in (0, 13, 63):
+            p, q = s2.posterior(k), e2.posterior(k)
+            assert float(np.max(np.abs(p - q) / np.maximum(np.abs(q), 1.0))) <= 1e-4
+
+
+def test_wide_rows_cfg3_with_saturation_path(cfg3_ensemble):
+    """Degree 13/14 rows (the 128-register instance) through the generic
+    (SAT) path: clamp 40, 32 frames, against the oracle."""
+    cfg = DecoderConfig(llr_clamp=40.0)
+    fb = make_frames(cfg3_ensemble.n, 0.03, 32, seed=61)
+    dec = BatchDecoder(cfg3_ensemble, 32, cfg)
+    syn = dec.syndromes(fb.keys)
+    res = dec.decode(fb.noisy, syn, 0.03)
+    frames = range(0, 32, 4)   # the oracle needs ~0.1 s per frame here
+    _assert_matches(res, _oracle_all(cfg3_ensemble, fb.noisy, syn, 0.03, cfg, frames), frames)
+
+
+@pytest.mark.parametrize("subbatches", ["1", "3", "8"])
+def test_host_path_pipelining_is_transparent(cfg2_ensemble, subbatches):
+    """mbp_decode_batch (host buffers) splits the batch into sub-batches whose
+    copies overlap the decode; results equal the device-buffer path."""
+    import torch
+
+    B = 512
+    fb = make_frames(cfg2_ensemble.n, 0.04, B, seed=71)
+    dec = BatchDecoder(cfg2_ensemble, B)
+    dev = torch.device("cuda:0")
+    syn_d = dec.syndromes(torch.from_numpy(fb.keys).to(dev))
+    ref = dec.decode_device(torch.from_numpy(fb.noisy).to(dev), syn_d, 0.04)
+    torch.cuda.synchronize()
+    old = os.environ.get("MBP_HOST_SUBBATCHES")
+    os.environ["MBP_HOST_SUBBATCHES"] = subbatches
+    try:
+        res = dec.decode(fb.noisy, syn_d.cpu().numpy(), 0.04)
+    finally:
+        if old is None:
+            del os.environ["MBP_HOST_SUBBATCHES"]
+        else:
+            os.environ["MBP_HOST_SUBBATCHES"] = old
+    assert np.array_equal(res.corrected, ref[0].cpu().numpy())
+    assert np.array_equal(res.converged, ref[1].cpu().numpy().astype(bool))
+    assert np.array_equal(res.iterations, ref[2].cpu().numpy())
+    assert np.array_equal(res.mismatches, ref[3].cpu().numpy())
+    good = res.converged & np.all(res.corrected == fb.keys, axis=1)
+    assert good.mean() > 0.99
