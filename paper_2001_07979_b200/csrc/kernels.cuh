@@ -215,79 +215,109 @@ constexpr int kDecodeThreads = 256;  // decode kernel block size (decode.cuh)
 // ---------------------------------------------------------------------------
 // bit-matrix transposes between BitBlock rows and 32-frame words
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ unsigned load_row_u32(const uint8_t* row, long long byte0, long long nbytes)
+// 32x32 bit transpose across a warp: in lane l holds row l; out lane l holds
+// column l (bit f of out = bit l of lane f's input).  Recursive block swap:
+// at stage j the lanes l and l^j exchange the j x j blocks off the diagonal
+// (5 shuffles instead of 32 ballots).
+__device__ __forceinline__ unsigned warp_transpose32(unsigned x, int lane)
 {
-    unsigned x = 0;
+    constexpr unsigned kM[5] = {0x0000ffffu, 0x00ff00ffu, 0x0f0f0f0fu, 0x33333333u, 0x55555555u};
 #pragma unroll
-    for (int b = 0; b < 4; ++b)
-        if (byte0 + b < nbytes) x |= (unsigned)row[byte0 + b] << (8 * b);
+    for (int q = 0; q < 5; ++q) {
+        const int j = 16 >> q;
+        const unsigned m = kM[q];
+        const unsigned y = __shfl_xor_sync(kFull, x, j);
+        x = (lane & j) ? ((x & ~m) | ((y & ~m) >> j)) : ((x & m) | ((y & m) << j));
+    }
     return x;
 }
 
-// 32x32 bit transpose across a warp: in lane l holds row l; out lane l holds
-// column l (bit f of out = bit l of lane f's input).
-__device__ __forceinline__ unsigned warp_transpose32(unsigned x, int lane)
+// Tiled transposes between BitBlock rows and 32-frame words.  A block owns
+// one tile: 32 rows (frames 32g..32g+31) x 128 bytes (1024 bits) of segment
+// s.  Rows are staged in shared memory with coalesced byte accesses (row
+// stride 132 B: the per-lane column reads below are bank-conflict free); each
+// warp converts 4 of the tile's 32 bit-chunks with ballot transposes and
+// writes whole 128-byte lines of words.
+constexpr int kTileBytes = 128;
+constexpr int kTileStride = kTileBytes + 4;
+
+// rows [B][row_bytes]: segment s = bytes [s*seg_bytes, +seg_bytes) holding
+// seg_bits bits -> words[g][s*seg_bits + bit] (and words2 if given)
+static __global__ void __launch_bounds__(256) rows_to_words_kernel(
+    const uint8_t* __restrict__ rows, long long row_bytes, int B, int G, int nseg, int seg_bits,
+    long long seg_bytes, unsigned* __restrict__ words, unsigned* __restrict__ words2, long long words_per_group)
 {
-    unsigned r = 0;
+    __shared__ __align__(16) uint8_t tile[32 * kTileStride];
+    const int tiles = (int)((seg_bytes + kTileBytes - 1) / kTileBytes);
+    const long long total = (long long)G * nseg * tiles;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (long long it = blockIdx.x; it < total; it += gridDim.x) {
+        const int xt = (int)(it % tiles);
+        const int s = (int)((it / tiles) % nseg);
+        const int g = (int)(it / ((long long)tiles * nseg));
+        const long long b0 = (long long)xt * kTileBytes;
+        uint8_t v[32 * kTileBytes / 256];   // all loads in flight before the stores
 #pragma unroll
-    for (int b = 0; b < 32; ++b) {
-        const unsigned w = __ballot_sync(kFull, (x >> b) & 1u);
-        if (lane == b) r = w;
+        for (int q = 0; q < 32 * kTileBytes / 256; ++q) {
+            const int idx = threadIdx.x + 256 * q;
+            const int r = idx / kTileBytes, b = idx % kTileBytes;
+            const int f = g * 32 + r;
+            v[q] = (f < B && b0 + b < seg_bytes) ? rows[(long long)f * row_bytes + (long long)s * seg_bytes + b0 + b] : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < 32 * kTileBytes / 256; ++q) {
+            const int idx = threadIdx.x + 256 * q;
+            tile[(idx / kTileBytes) * kTileStride + idx % kTileBytes] = v[q];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int c = warp + 8 * q;   // 32-bit chunk of the tile
+            const unsigned x = *reinterpret_cast<const unsigned*>(tile + lane * kTileStride + 4 * c);
+            const unsigned w = warp_transpose32(x, lane);
+            const long long bit = b0 * 8 + 32LL * c + lane;
+            if (bit < seg_bits) {
+                const long long o = (long long)g * words_per_group + (long long)s * seg_bits + bit;
+                words[o] = w;
+                if (words2) words2[o] = w;
+            }
+        }
+        __syncthreads();
     }
-    return r;
 }
 
-// rows [B][row_bytes], bits [seg_off*8 + 32c, +32) of segment s of each row ->
-// words[g][word_off + 32c + lane].  grid-stride over (g, segment, chunk).
-static __global__ void rows_to_words_kernel(const uint8_t* __restrict__ rows, long long row_bytes, int B,
-                                     int G, int nseg, int seg_bits, long long seg_bytes,
-                                     unsigned* __restrict__ words, unsigned* __restrict__ words2,
-                                     long long words_per_group)
+// words[g][s*seg_bits + bit] -> rows (inverse of rows_to_words_kernel); row
+// padding bits come out zero because words past seg_bits read as 0
+static __global__ void __launch_bounds__(256) words_to_rows_kernel(
+    const unsigned* __restrict__ words, long long words_per_group, int B, int G, int nseg, int seg_bits,
+    long long seg_bytes, uint8_t* __restrict__ rows, long long row_bytes)
 {
-    const int lane = threadIdx.x & 31;
-    const int chunks = (seg_bits + 31) / 32;
-    const long long total = (long long)G * nseg * chunks;
-    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
-    for (long long it = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < total; it += nw) {
-        const int c = (int)(it % chunks);
-        const int s = (int)((it / chunks) % nseg);
-        const int g = (int)(it / ((long long)chunks * nseg));
-        const int f = g * 32 + lane;
-        unsigned x = 0;
-        if (f < B) x = load_row_u32(rows + (long long)f * row_bytes + (long long)s * seg_bytes, 4LL * c, seg_bytes);
-        const unsigned w = warp_transpose32(x, lane);
-        const int bit = 32 * c + lane;
-        if (bit < seg_bits) {
-            const long long o = (long long)g * words_per_group + (long long)s * seg_bits + bit;
-            words[o] = w;
-            if (words2) words2[o] = w;
-        }
-    }
-}
-
-// words[g][word_off + 32c + lane] -> rows (inverse of rows_to_words_kernel)
-static __global__ void words_to_rows_kernel(const unsigned* __restrict__ words, long long words_per_group,
-                                     int B, int G, int nseg, int seg_bits, long long seg_bytes,
-                                     uint8_t* __restrict__ rows, long long row_bytes)
-{
-    const int lane = threadIdx.x & 31;
-    const int chunks = (seg_bits + 31) / 32;
-    const long long total = (long long)G * nseg * chunks;
-    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
-    for (long long it = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < total; it += nw) {
-        const int c = (int)(it % chunks);
-        const int s = (int)((it / chunks) % nseg);
-        const int g = (int)(it / ((long long)chunks * nseg));
-        const int bit = 32 * c + lane;
-        const unsigned w = bit < seg_bits ? words[(long long)g * words_per_group + (long long)s * seg_bits + bit] : 0u;
-        const unsigned x = warp_transpose32(w, lane);
-        const int f = g * 32 + lane;
-        if (f < B) {
-            uint8_t* r = rows + (long long)f * row_bytes + (long long)s * seg_bytes;
+    __shared__ __align__(16) uint8_t tile[32 * kTileStride];
+    const int tiles = (int)((seg_bytes + kTileBytes - 1) / kTileBytes);
+    const long long total = (long long)G * nseg * tiles;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (long long it = blockIdx.x; it < total; it += gridDim.x) {
+        const int xt = (int)(it % tiles);
+        const int s = (int)((it / tiles) % nseg);
+        const int g = (int)(it / ((long long)tiles * nseg));
+        const long long b0 = (long long)xt * kTileBytes;
 #pragma unroll
-            for (int b = 0; b < 4; ++b)
-                if (4LL * c + b < seg_bytes) r[4LL * c + b] = (uint8_t)(x >> (8 * b));
+        for (int q = 0; q < 4; ++q) {
+            const int c = warp + 8 * q;
+            const long long bit = b0 * 8 + 32LL * c + lane;
+            const unsigned w = bit < seg_bits ? words[(long long)g * words_per_group + (long long)s * seg_bits + bit] : 0u;
+            *reinterpret_cast<unsigned*>(tile + lane * kTileStride + 4 * c) = warp_transpose32(w, lane);
         }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 32 * kTileBytes / 256; ++q) {
+            const int idx = threadIdx.x + 256 * q;
+            const int r = idx / kTileBytes, b = idx % kTileBytes;
+            const int f = g * 32 + r;
+            if (f < B && b0 + b < seg_bytes)
+                rows[(long long)f * row_bytes + (long long)s * seg_bytes + b0 + b] = tile[r * kTileStride + b];
+        }
+        __syncthreads();
     }
 }
 
@@ -304,7 +334,15 @@ static __global__ void syndrome_words_kernel(const uint8_t* __restrict__ deg, co
         const unsigned* kw = key_w + (long long)g * n;
         const int* row = chk_ell + (long long)j * D;
         unsigned p = 0;
-        for (int k = 0, d = __ldg(deg + j); k < d; ++k) p ^= __ldg(kw + __ldg(row + k));
+        const int d = __ldg(deg + j);
+        for (int k0 = 0; k0 < d; k0 += 8) {   // 8 row loads, then 8 word loads, in flight
+            int id[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) id[k] = k0 + k < d ? __ldg(row + k0 + k) : -1;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (id[k] >= 0) p ^= __ldg(kw + id[k]);
+        }
         syn_w[it] = p;
     }
 }

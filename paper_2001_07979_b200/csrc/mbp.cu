@@ -420,19 +420,14 @@ int mbp_workspace_configure(mbp_workspace* ws, const mbp_decoder_config* cfg)
 // ---------------------------------------------------------------------------
 // launch helpers
 // ---------------------------------------------------------------------------
-static int grid_for(long long warps_needed)
-{
-    long long blocks = (warps_needed + 7) / 8;
-    return (int)std::max(1LL, std::min(blocks, 148LL * 16));
-}
-
 static int launch_rows_to_words(const uint8_t* rows, long long row_bytes, int B, int G, int nseg,
                                 int seg_bits, long long seg_bytes, unsigned* words, unsigned* words2,
                                 long long wpg, cudaStream_t s)
 {
-    const long long items = (long long)G * nseg * ((seg_bits + 31) / 32);
-    mbp::rows_to_words_kernel<<<grid_for(items), 256, 0, s>>>(rows, row_bytes, B, G, nseg, seg_bits,
-                                                               seg_bytes, words, words2, wpg);
+    const long long tiles = (long long)G * nseg * ((seg_bytes + mbp::kTileBytes - 1) / mbp::kTileBytes);
+    const int grid = (int)std::max(1LL, std::min(tiles, 148LL * 8));
+    mbp::rows_to_words_kernel<<<grid, 256, 0, s>>>(rows, row_bytes, B, G, nseg, seg_bits, seg_bytes, words,
+                                                   words2, wpg);
     MBP_CUDA(cudaGetLastError());
     return MBP_OK;
 }
@@ -441,9 +436,9 @@ static int launch_words_to_rows(const unsigned* words, long long wpg, int B, int
                                 int seg_bits, long long seg_bytes, uint8_t* rows, long long row_bytes,
                                 cudaStream_t s)
 {
-    const long long items = (long long)G * nseg * ((seg_bits + 31) / 32);
-    mbp::words_to_rows_kernel<<<grid_for(items), 256, 0, s>>>(words, wpg, B, G, nseg, seg_bits, seg_bytes,
-                                                              rows, row_bytes);
+    const long long tiles = (long long)G * nseg * ((seg_bytes + mbp::kTileBytes - 1) / mbp::kTileBytes);
+    const int grid = (int)std::max(1LL, std::min(tiles, 148LL * 8));
+    mbp::words_to_rows_kernel<<<grid, 256, 0, s>>>(words, wpg, B, G, nseg, seg_bits, seg_bytes, rows, row_bytes);
     MBP_CUDA(cudaGetLastError());
     return MBP_OK;
 }

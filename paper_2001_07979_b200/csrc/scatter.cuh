@@ -574,7 +574,7 @@ __device__ __forceinline__ void sc_var_chunk(const ScatterArgs& A, const SL<CPT>
 // ---------------------------------------------------------------------------
 // syndrome phase (mismatch_count, _kernels.py:310-320): 32 consecutive checks
 // of group g per warp item (lane = check); the mismatch word (bit f = frame
-// f) becomes per-frame counts via 32 ballots, returned in lane f.  At t = 0
+// f) becomes per-frame counts via a bit transpose + popc, returned in lane f.  At t = 0
 // the full mismatch words are stored (the sweep-1 message signs).  Callers
 // accumulate counts over their chunk and flush once per group: per-item
 // atomics on the 32 counters of a group all land on one L2 line and
@@ -604,15 +604,8 @@ __device__ __forceinline__ int sc_syncheck_item(const ScatterArgs& A, const SL<C
         if (t == 0) S.mis()[(size_t)g * A.C + j] = full;
         mism = full & act;
     }
-    int c = 0;
-    if (__any_sync(kFull, mism != 0)) {
-#pragma unroll
-        for (int f = 0; f < 32; ++f) {
-            const int pc = __popc(__ballot_sync(kFull, (mism >> f) & 1u));
-            if (lane == f) c = pc;
-        }
-    }
-    return c;
+    // lane f: popcount of bit f over the 32 checks = transpose, then popc
+    return __any_sync(kFull, mism != 0) ? __popc(warp_transpose32(mism, lane)) : 0;
 }
 
 // items per claim: about one claim per warp (few flushes per group line),
