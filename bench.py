@@ -169,12 +169,17 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples), "source": self.source}
 
 
-def load_workload(rank, frames, e):
+def load_workload(rank, frames, e, world=1):
+    """Rank's shard of the frame stream: frames [rank*B, (rank+1)*B) of the
+    reference's counter-based streams (shard.shard_range over world*B frames,
+    weak scaling: B frames per GPU)."""
     from paper_2001_07979_b200.channel import make_frames
     from paper_2001_07979_b200.matrix import load_ensemble
+    from paper_2001_07979_b200.shard import shard_range
 
     ens = load_ensemble(ENS_FILE)
-    fb = make_frames(ens.n, e, frames, seed=0, start=rank * frames)
+    lo, hi = shard_range(world * frames, world, rank)
+    fb = make_frames(ens.n, e, hi - lo, seed=0, start=lo)
     return ens, fb
 
 
@@ -271,7 +276,7 @@ def main():
 
     from paper_2001_07979_b200 import BatchDecoder, DecoderConfig
 
-    ens, fb = load_workload(rank, args.frames, args.e)
+    ens, fb = load_workload(rank, args.frames, args.e, world)
     n, m, u = ens.n, ens.m, ens.u
     B = fb.batch
     dec = BatchDecoder(ens, B, DecoderConfig(precision=args.precision), device=local)
@@ -338,21 +343,11 @@ def main():
     e2e_good = int((res.converged & np.all(res.corrected == fb.keys, axis=1)).sum()) * n
     e2e_total_ms = sum(e2e_ms)
 
-    # ---- cross-rank aggregation: sums of work, max of time -------------------
-    vals = torch.tensor([good_bits, total_ms, e2e_good * e2e_steps, e2e_total_ms, float(B)],
-                        dtype=torch.float64, device=dev)
-    if world > 1:
-        import torch.distributed as dist
+    # ---- cross-rank aggregation: sums of work, max of time (shard.py) --------
+    from paper_2001_07979_b200.shard import reduce_work_time
 
-        sums = vals.clone()
-        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
-        maxs = vals.clone()
-        dist.all_reduce(maxs, op=dist.ReduceOp.MAX)
-        good_bits_all, e2e_good_all, frames_all = sums[0].item(), sums[2].item(), sums[4].item()
-        total_ms_max, e2e_ms_max = maxs[1].item(), maxs[3].item()
-    else:
-        good_bits_all, e2e_good_all, frames_all = float(good_bits), float(e2e_good * e2e_steps), float(B)
-        total_ms_max, e2e_ms_max = total_ms, e2e_total_ms
+    (good_bits_all, e2e_good_all, frames_all), (total_ms_max, e2e_ms_max) = reduce_work_time(
+        [float(good_bits), float(e2e_good * e2e_steps), float(B)], [total_ms, e2e_total_ms], device=dev)
 
     value = good_bits_all / (total_ms_max / 1e3) / 1e6
     e2e_value = e2e_good_all / (e2e_ms_max / 1e3) / 1e6
