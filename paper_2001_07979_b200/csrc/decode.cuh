@@ -279,14 +279,19 @@ __device__ __forceinline__ void var_item(const DecodeArgs<Real>& A, const L<Real
     }
 }
 
+__device__ __forceinline__ unsigned group_mask(const int* cprev, int g, int lane)
+{
+    return __ballot_sync(kFull, ld_cg(cprev + g * 32 + lane) != 0);
+}
+
 // ---------------------------------------------------------------------------
 // syndrome phase: 32 consecutive checks (lane = check) of group g.  Mismatch
 // words (bit f = frame f) become per-frame counts via 32 ballots, added to
 // cnt[t&1].
 // ---------------------------------------------------------------------------
 template <class Real, bool CPT>
-__device__ __forceinline__ void syncheck_item(const DecodeArgs<Real>& A, const L<Real, CPT>& S, int g, int blk,
-                                              int t, unsigned act, int lane)
+__device__ __forceinline__ int syncheck_item(const DecodeArgs<Real>& A, const L<Real, CPT>& S, int g, int blk,
+                                             int t, unsigned act, int lane)
 {
     const int j = blk * 32 + lane;
     unsigned mism = 0;
@@ -298,14 +303,35 @@ __device__ __forceinline__ void syncheck_item(const DecodeArgs<Real>& A, const L
         for (int k = 0; k < d; ++k) par ^= ld_cg(hw + ld_ro(row + k));
         mism = (par ^ S.syn((size_t)g * A.C + j)) & act;
     }
+    // lane f: popcount of bit f over the 32 checks (bit transpose + popc)
+    return __any_sync(kFull, mism != 0) ? __popc(warp_transpose32(mism, lane)) : 0;
+}
+
+// A claimed run of syndrome items; per-frame counts accumulate in registers
+// and are flushed once per group (per-item atomics on a group's 32 counters
+// all hit one L2 line and serialise).
+template <class Real, bool CPT>
+__device__ __forceinline__ void syncheck_run(const DecodeArgs<Real>& A, const L<Real, CPT>& S, int base, int end,
+                                             int t, const int* cprev, int cblk, int lane)
+{
+    int g = base / cblk;
+    unsigned act = cprev ? group_mask(cprev, g, lane) : kFull;
     int c = 0;
-#pragma unroll
-    for (int f = 0; f < 32; ++f) {
-        const int pc = __popc(__ballot_sync(kFull, (mism >> f) & 1u));
-        if (lane == f) c = pc;
+    bool bad = false;
+    for (int item = base; item < end; ++item) {
+        const int gi = item / cblk;
+        if (gi != g) {
+            if (c) atomicAdd(S.cnt() + (t & 1) * S.G * 32 + g * 32 + lane, c);
+            bad |= c != 0;
+            c = 0;
+            g = gi;
+            act = cprev ? group_mask(cprev, g, lane) : kFull;
+        }
+        if (act) c += syncheck_item<Real, CPT>(A, S, g, item - g * cblk, t, act, lane);
     }
     if (c) atomicAdd(S.cnt() + (t & 1) * S.G * 32 + g * 32 + lane, c);
-    if (__any_sync(kFull, c != 0) && lane == 0) atomicOr(A.any_bad + (t & 1), 1);
+    bad |= c != 0;
+    if (__any_sync(kFull, bad) && lane == 0) atomicOr(A.any_bad + (t & 1), 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -355,10 +381,7 @@ __device__ __forceinline__ int claim(unsigned* counter, int lane, int n)
     return (int)__shfl_sync(kFull, base, 0);
 }
 
-__device__ __forceinline__ unsigned group_mask(const int* cprev, int g, int lane)
-{
-    return __ballot_sync(kFull, ld_cg(cprev + g * 32 + lane) != 0);
-}
+
 
 // one claimed chunk of the check phase: items [base, end) of the G*C space
 // input row base of c2v_{t-1} for lane `lane` of group g (see check_item)
@@ -643,17 +666,9 @@ __device__ __forceinline__ void sweep_phases(const DecodeArgs<Real>& A, int G, i
     stamp(A, ts_k);
     {   // syndrome phase
         const int total = G * cblk;
-        for (int base = claim(A.work + wc, lane, kSynChunk); base < total;
-             base = claim(A.work + wc, lane, kSynChunk)) {
-            const int end = min(base + kSynChunk, total);
-            int g = base / cblk;
-            unsigned act = group_mask(cp, g, lane);
-            for (int item = base; item < end; ++item) {
-                const int gi = item / cblk;
-                if (gi != g) { g = gi; act = group_mask(cp, g, lane); }
-                if (act) syncheck_item<Real, CPT>(A, S, g, item - g * cblk, t, act, lane);
-            }
-        }
+        const int sc = min(64, max(8, (total + nwarps - 1) / nwarps));   // ~one claim per warp
+        for (int base = claim(A.work + wc, lane, sc); base < total; base = claim(A.work + wc, lane, sc))
+            syncheck_run<Real, CPT>(A, S, base, min(base + sc, total), t, cp, cblk, lane);
         ++wc;
     }
 }
@@ -700,10 +715,9 @@ decode_kernel(const DecodeArgs<Real> A)
     {
         const L<Real, false> S0{A, A.G};
         const int total = A.G * cblk;
-        for (int base = claim(A.work + wc, lane, kSynChunk); base < total;
-             base = claim(A.work + wc, lane, kSynChunk))
-            for (int item = base; item < min(base + kSynChunk, total); ++item)
-                syncheck_item<Real, false>(A, S0, item / cblk, item % cblk, 0, kFull, lane);
+        const int sc = min(64, max(8, (total + nwarps - 1) / nwarps));
+        for (int base = claim(A.work + wc, lane, sc); base < total; base = claim(A.work + wc, lane, sc))
+            syncheck_run<Real, false>(A, S0, base, min(base + sc, total), 0, nullptr, cblk, lane);
         ++wc;
     }
 

@@ -224,11 +224,13 @@ __device__ __forceinline__ void rule_sd(const float (&x)[DD], int d, unsigned fl
 // first gather (post'_{s0-1}) of the next row is issued before the current
 // row's rule (software pipeline).  FULL: every lane of the group is live.
 // ---------------------------------------------------------------------------
-template <int D, int DD, bool PAD, bool FULL, bool SAT, bool T2, bool CPT>
+template <int D, int DD, bool PAD, bool FULL, bool SAT, bool T2, bool CPT, bool C3 = false>
 __device__ __forceinline__ void sc_row(const ScatterArgs& A, const SL<CPT>& S, const float (&p)[D], int d,
                                        unsigned sj, float M1, const unsigned* soff, bool live, int t_,
-                                       const float* gb, const float* qrow, float* crow, float scale, bool absolute)
+                                       const float* gb, const float* qrow, float* crow, float scale, bool absolute,
+                                       const float (&p2)[D])
 {
+    // C3: sweep 3 with the rebuilt chain, post'_2 values prefetched by the caller
     // T2: sweep 2, the hot case (no chain, no store) compiled on its own
     const int t = T2 ? 2 : t_;
     const bool lv = FULL || live;
@@ -263,8 +265,14 @@ __device__ __forceinline__ void sc_row(const ScatterArgs& A, const SL<CPT>& S, c
             const float* gs = gb + ((s - 1) & 1) * 32;   // post'_{s-1} line
 #pragma unroll
             for (int k = 0; k < DD; ++k) {
-                const float* q = byte_off(gs, soff[k]);
-                x[k] = (FULL ? ld_cg(q) : ld_cg_if(q, live)) - c[k];
+                float pv;
+                if constexpr (C3) {
+                    pv = p2[k];
+                } else {
+                    const float* q = byte_off(gs, soff[k]);
+                    pv = FULL ? ld_cg(q) : ld_cg_if(q, live);
+                }
+                x[k] = pv - c[k];
                 if (s == t) vold[k] = __float2int_rn(c[k] * scale);
             }
             rule_sd<DD, PAD, SAT>(x, d, sj, A.clamp, A.sat, c);
@@ -297,30 +305,39 @@ __device__ __forceinline__ const float* sc_c2v_in_base(const ScatterArgs& A, con
 }
 
 // rows [r0, r1) of the staged chunk, all in group g (first row j0)
-template <int D, bool FULL, bool SAT, bool T2, bool CPT>
+template <int D, bool FULL, bool SAT, bool T2, bool CPT, bool C3 = false>
 __device__ __forceinline__ void sc_span(const ScatterArgs& A, const SL<CPT>& S, int g, int j0, int r0, int r1, int t,
                                         unsigned act, int lane, const unsigned* s_off, const unsigned* s_m,
                                         const int* s_d, const float* s_m1, bool first, float scale)
 {
     constexpr int SD = Chunk<D>::SD;
     if (T2) t = 2;
+    if (C3) t = 3;
     const bool live = (act >> lane) & 1u;
     const bool explicit_base = !T2 && t > kStoreFrom;
     const float* gb = S.vrow((size_t)g * A.n, lane);
     const float* qb = explicit_base ? sc_c2v_in_base<CPT>(A, S, g, lane, first) : nullptr;
     // first gather: post'_{s0-1}
     const float* gf = gb + (((explicit_base ? t : 2) - 1) & 1) * 32;
-    float pn[D];
+    const float* g2 = gb;    // post'_2 line (C3)
+    float pn[D], pn2[C3 ? D : 1];
 #pragma unroll
     for (int k = 0; k < D; ++k) {
         const float* q = byte_off(gf, s_off[r0 * SD + k]);
         pn[k] = FULL ? ld_cg(q) : ld_cg_if(q, live);
+        if constexpr (C3) {
+            const float* q2 = byte_off(g2, s_off[r0 * SD + k]);
+            pn2[k] = FULL ? ld_cg(q2) : ld_cg_if(q2, live);
+        }
     }
     int dn = s_d[r0];
     for (int r = r0; r < r1; ++r) {
-        float p[D];
+        float p[D], p2[D];
 #pragma unroll
-        for (int k = 0; k < D; ++k) p[k] = pn[k];
+        for (int k = 0; k < D; ++k) {
+            p[k] = pn[k];
+            if constexpr (C3) p2[k] = pn2[k];
+        }
         const int d = dn;
         if (r + 1 < r1) {
             dn = s_d[r + 1];
@@ -328,6 +345,10 @@ __device__ __forceinline__ void sc_span(const ScatterArgs& A, const SL<CPT>& S, 
             for (int k = 0; k < D; ++k) {
                 const float* q = byte_off(gf, s_off[(r + 1) * SD + k]);
                 pn[k] = FULL ? ld_cg(q) : ld_cg_if(q, live);
+                if constexpr (C3) {
+                    const float* q2 = byte_off(g2, s_off[(r + 1) * SD + k]);
+                    pn2[k] = FULL ? ld_cg(q2) : ld_cg_if(q2, live);
+                }
             }
         }
         const unsigned sj = (s_m[r] >> lane) & 1u;
@@ -341,12 +362,14 @@ __device__ __forceinline__ void sc_span(const ScatterArgs& A, const SL<CPT>& S, 
         const float* qrow = explicit_base ? qb + (size_t)j * A.Ds * 32 : nullptr;
         float* crow = t >= kStoreFrom ? S.c2v() + ((size_t)g * A.slots + (size_t)j * A.Ds) * 32 + lane : nullptr;
         if (d == D)
-            sc_row<D, D, false, FULL, SAT, T2, CPT>(A, S, p, d, sj, M1, soff, live, t, gb, qrow, crow, scale, first);
+            sc_row<D, D, false, FULL, SAT, T2, CPT, C3>(A, S, p, d, sj, M1, soff, live, t, gb, qrow, crow, scale,
+                                                        first, p2);
         else if (D > 1 && d == D - 1)
-            sc_row<D, (D > 1 ? D - 1 : 1), false, FULL, SAT, T2, CPT>(A, S, p, d, sj, M1, soff, live, t, gb, qrow,
-                                                                      crow, scale, first);
+            sc_row<D, (D > 1 ? D - 1 : 1), false, FULL, SAT, T2, CPT, C3>(A, S, p, d, sj, M1, soff, live, t, gb,
+                                                                          qrow, crow, scale, first, p2);
         else
-            sc_row<D, D, true, FULL, SAT, T2, CPT>(A, S, p, d, sj, M1, soff, live, t, gb, qrow, crow, scale, first);
+            sc_row<D, D, true, FULL, SAT, T2, CPT, C3>(A, S, p, d, sj, M1, soff, live, t, gb, qrow, crow, scale,
+                                                       first, p2);
     }
 }
 
@@ -389,6 +412,9 @@ __device__ __forceinline__ void sc_check_chunk(const ScatterArgs& A, const SL<CP
                 if (t == 2)
                     sc_span<D, true, false, true, CPT>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d, s_m1,
                                                        first, scale);
+                else if (t == 3 && kStoreFrom == 3)
+                    sc_span<D, true, false, false, CPT, true>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d,
+                                                              s_m1, first, scale);
                 else
                     sc_span<D, true, false, false, CPT>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d,
                                                         s_m1, first, scale);
