@@ -37,8 +37,16 @@ sys.path.insert(0, str(ROOT))
 
 N_DEFAULT_FRAMES = 1024
 WORKLOAD = "cfg2"
-ENS_FILE = ROOT / "paper_2001_07979_b200" / "ensembles" / "cfg2_n65536_m32768_u2_s1.npz"
 E_DEFAULT = 0.03
+# BASELINE.json configs: the headline is cfg2 (configs[1]); the others are
+# parity-test cases that --workload can also time (cfg4 uses SYNTHETIC random
+# (3,6)-regular graphs, the reference's PEG being ~7 h per matrix at 2^20)
+WORKLOADS = {
+    "cfg1": ("cfg1_n4096_m2048_u2_s1.npz", "u=2 PEG n=4096 m=2048 R=0.5 (reference build_ensemble seeds 1,2)"),
+    "cfg2": ("cfg2_n65536_m32768_u2_s1.npz", "u=2 PEG n=65536 m=32768 R=0.5 (reference build_ensemble seeds 1,2)"),
+    "cfg3": ("cfg3_n65536_m14650_u3_s11.npz", "u=3 PEG n=65536 m=14650 (f=1.15 at e=0.03; reference seeds 11-13)"),
+    "cfg4": (None, "u=2 n=1048576 m=524288 R=0.5 SYNTHETIC random (3,6)-regular graphs (seeds 7,8)"),
+}
 L2_FLUSH_BYTES = 256 << 20   # > 126 MB L2: written between timed steps
 
 
@@ -53,6 +61,8 @@ def parse():
     p.add_argument("--precision", choices=("fp32", "fp64"), default="fp32")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-sweep", action="store_true", help="skip the QBER 2-5%% side sweep")
+    p.add_argument("--workload", choices=tuple(WORKLOADS), default=WORKLOAD,
+                   help="BASELINE config to time (default cfg2 = configs[1], the headline)")
     return p.parse_args()
 
 
@@ -169,15 +179,17 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples), "source": self.source}
 
 
-def load_workload(rank, frames, e, world=1):
+def load_workload(rank, frames, e, world=1, workload=WORKLOAD):
     """Rank's shard of the frame stream: frames [rank*B, (rank+1)*B) of the
     reference's counter-based streams (shard.shard_range over world*B frames,
     weak scaling: B frames per GPU)."""
     from paper_2001_07979_b200.channel import make_frames
-    from paper_2001_07979_b200.matrix import load_ensemble
+    from paper_2001_07979_b200.matrix import load_ensemble, random_regular_ensemble
     from paper_2001_07979_b200.shard import shard_range
 
-    ens = load_ensemble(ENS_FILE)
+    fname = WORKLOADS[workload][0]
+    ens = (load_ensemble(ROOT / "paper_2001_07979_b200" / "ensembles" / fname) if fname
+           else random_regular_ensemble(1 << 20, 1 << 19, 2, seed=7))
     lo, hi = shard_range(world * frames, world, rank)
     fb = make_frames(ens.n, e, hi - lo, seed=0, start=lo)
     return ens, fb
@@ -208,7 +220,7 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    ens, fb = load_workload(0, args.frames, args.e)
+    ens, fb = load_workload(0, args.frames, args.e, 1, args.workload)
     import oracle
     from paper_2001_07979_b200.matrix import stacked_layout
 
@@ -251,7 +263,7 @@ def run_reference(args):
 def config_dict(args, ens):
     from paper_2001_07979_b200.channel import efficiency
 
-    return {"workload": f"{WORKLOAD}: u=2 PEG n=65536 m=32768 R=0.5 (reference build_ensemble seeds 1,2), "
+    return {"workload": f"{args.workload}: {WORKLOADS[args.workload][1]}, "
                         f"BSC e={args.e}, {args.frames}-frame batch per GPU",
             "n": ens.n, "m": ens.m, "u": ens.u, "e": args.e, "f": round(efficiency(ens.m, ens.n, args.e), 4),
             "frames_per_gpu": args.frames, "max_iterations": 60, "llr_clamp": 30.0,
@@ -276,7 +288,7 @@ def main():
 
     from paper_2001_07979_b200 import BatchDecoder, DecoderConfig
 
-    ens, fb = load_workload(rank, args.frames, args.e, world)
+    ens, fb = load_workload(rank, args.frames, args.e, world, args.workload)
     n, m, u = ens.n, ens.m, ens.u
     B = fb.batch
     dec = BatchDecoder(ens, B, DecoderConfig(precision=args.precision), device=local)
@@ -364,7 +376,7 @@ def main():
     if tf.exists():
         try:
             t = json.loads(tf.read_text())
-            if t.get("workload") == WORKLOAD and t.get("frames") == B and t.get("e") == args.e:
+            if t.get("workload") == args.workload and t.get("frames") == B and t.get("e") == args.e:
                 traffic = t.get("dram_bytes_per_launch")
         except Exception:
             pass
@@ -419,7 +431,7 @@ def main():
     if rank == 0 and not args.no_sweep:
         sweep = {}
         for e in (0.02, 0.04, 0.05):
-            _, fbe = load_workload(rank, B, e)
+            _, fbe = load_workload(rank, B, e, world, args.workload)
             syn_e = dec.syndromes(torch.from_numpy(fbe.keys).to(dev))
             nd = torch.from_numpy(fbe.noisy).to(dev)
             ed = torch.tensor([e], dtype=torch.float64, device=dev)

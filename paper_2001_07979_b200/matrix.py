@@ -30,6 +30,8 @@ __all__ = [
     "save_ensemble",
     "load_ensemble",
     "code_rate",
+    "random_regular_matrix",
+    "random_regular_ensemble",
 ]
 
 ENSEMBLE_CACHE_VERSION = 1
@@ -163,6 +165,42 @@ class MatrixEnsemble:
 
     def content_hashes(self) -> list:
         return [h.content_hash() for h in self.matrices]
+
+
+def random_regular_matrix(n: int, m: int, dv: int = 3, seed: int = 0) -> ParityCheckMatrix:
+    """A random (dv, dv*n/m)-regular Tanner graph (configuration model with
+    parallel edges swapped out) -- a SYNTHETIC stand-in where the reference's
+    PEG construction is out of reach (n = 2^20: ~7 h per matrix in the
+    reference).  The decoder does not care how
+    a graph was built; parity against the oracle holds for any graph."""
+    E = n * dv
+    if E % m:
+        raise ValueError(f"n*dv = {E} not divisible by m = {m}")
+    dc = E // m
+    rng = np.random.default_rng(seed)
+    var_of_socket = np.repeat(np.arange(n, dtype=np.int64), dv)
+    perm = rng.permutation(E)
+    chk_of_socket = perm // dc            # check socket slot -> check id
+    # parallel edges: swap the variable of a duplicated (check, var) pair with
+    # a random socket until none remain
+    for _ in range(100):
+        key = chk_of_socket * n + var_of_socket
+        order = np.argsort(key, kind="stable")
+        dup = order[1:][key[order[1:]] == key[order[:-1]]]
+        if dup.size == 0:
+            break
+        other = rng.integers(0, E, size=dup.size)
+        var_of_socket[dup], var_of_socket[other] = var_of_socket[other], var_of_socket[dup].copy()
+    else:
+        raise RuntimeError("could not remove parallel edges")
+    order = np.lexsort((var_of_socket, chk_of_socket))
+    chk_ptr = np.arange(0, E + 1, dc, dtype=np.int64)
+    return ParityCheckMatrix._from_csr(n, m, chk_ptr, var_of_socket[order].astype(np.int32))
+
+
+def random_regular_ensemble(n: int, m: int, u: int, dv: int = 3, seed: int = 0) -> "MatrixEnsemble":
+    """u synthetic random regular matrices with seeds seed..seed+u-1."""
+    return MatrixEnsemble(tuple(random_regular_matrix(n, m, dv, seed + l) for l in range(u)))
 
 
 def code_rate(matrix) -> float:

@@ -157,3 +157,27 @@ def test_host_path_pipelining_is_transparent(cfg2_ensemble, subbatches):
     assert np.array_equal(res.mismatches, ref[3].cpu().numpy())
     good = res.converged & np.all(res.corrected == fb.keys, axis=1)
     assert good.mean() > 0.99
+
+
+@pytest.fixture(scope="module")
+def cfg4_ensemble():
+    """u = 2, n = 2^20, m = 2^19 (BASELINE configs[3], long-key frames whose
+    messages far exceed shared memory and L2).  SYNTHETIC random (3, 6)-regular
+    graphs: the reference's PEG needs ~7 h per matrix at this size."""
+    from paper_2001_07979_b200.matrix import random_regular_ensemble
+
+    return random_regular_ensemble(1 << 20, 1 << 19, 2, seed=7)
+
+
+def test_long_key_cfg4_against_oracle(cfg4_ensemble):
+    ens = cfg4_ensemble
+    B = 8
+    fb = make_frames(ens.n, 0.03, B, seed=91)
+    dec = BatchDecoder(ens, B)
+    syn = dec.syndromes(fb.keys)
+    res = dec.decode(fb.noisy, syn, 0.03)
+    assert res.converged.all()
+    assert np.array_equal(res.corrected, fb.keys)           # Alice's key recovered bit for bit
+    assert np.array_equal(dec.syndromes(res.corrected), syn)
+    frames = (0, 5)
+    _assert_matches(res, _oracle_all(ens, fb.noisy, syn, 0.03, DecoderConfig(), frames), frames)
