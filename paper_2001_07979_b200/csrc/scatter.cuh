@@ -517,25 +517,68 @@ __device__ __forceinline__ void sc_var1_chunk(const ScatterArgs& A, const SL<CPT
             __syncwarp();
             const bool live = (act >> lane) & 1u;
             const int Lf = S.Lfix(g * 32 + lane);
-            for (int v = r; v < r + span; ++v) {
-                const size_t w = (size_t)base + v;
-                const unsigned yw = s_y[v];
-                const unsigned y = (yw >> lane) & 1u;
-                int a = Lf;
+            const unsigned lbit = 1u << lane;
+            if (act == kFull && !A.hist_w) {
+                // every lane live, no history: two variables per pass, no predicates
+                int v = r;
+                for (; v + 1 < r + span; v += 2) {
+                    int a0 = Lf, a1 = Lf;
 #pragma unroll
-                for (int k = 0; k < DV; ++k) {
-                    const unsigned mw = s_mis[v * DV + k];
-                    const int mf = s_mf[s_deg[v * DV + k] * 32 + lane];
-                    a += ((mw >> lane) & 1u) ? -mf : mf;
+                    for (int k = 0; k < DV; ++k) {
+                        const int m0 = s_mf[s_deg[v * DV + k] * 32 + lane];
+                        const int m1 = s_mf[s_deg[(v + 1) * DV + k] * 32 + lane];
+                        a0 += (s_mis[v * DV + k] & lbit) ? -m0 : m0;
+                        a1 += (s_mis[(v + 1) * DV + k] & lbit) ? -m1 : m1;
+                    }
+                    const size_t w = (size_t)base + v;
+                    float* vr = S.vrow(w, lane);
+                    vr[32] = (float)a0 * iscale;
+                    reinterpret_cast<int*>(vr)[64] = a0;   // acc = post'_1 in fixed point
+                    vr[kVB + 32] = (float)a1 * iscale;
+                    reinterpret_cast<int*>(vr)[kVB + 64] = a1;
+                    const unsigned y0 = s_y[v] & lbit, y1 = s_y[v + 1] & lbit;
+                    const unsigned n0 = __ballot_sync(kFull, y0 ? a0 > 0 : a0 < 0);
+                    const unsigned n1 = __ballot_sync(kFull, y1 ? a1 > 0 : a1 < 0);
+                    if (lane == 0) {
+                        S.hard_w()[w] = n0;
+                        S.hard_w()[w + 1] = n1;
+                    }
                 }
-                float* vr = S.vrow(w, lane);
-                st_if(vr + 32, (float)a * iscale, live);
-                if (live) reinterpret_cast<int*>(vr)[64] = a;   // acc = post'_1 in fixed point
-                const unsigned neg = __ballot_sync(kFull, y ? a > 0 : a < 0);
-                if (lane == 0) {
-                    const unsigned hw = (neg & act) | (yw & ~act);
-                    S.hard_w()[w] = hw;
-                    if (A.hist_w) A.hist_w[((size_t)1 * A.G) * A.n + w] = hw;
+                if (v < r + span) {
+                    int a0 = Lf;
+#pragma unroll
+                    for (int k = 0; k < DV; ++k) {
+                        const int m0 = s_mf[s_deg[v * DV + k] * 32 + lane];
+                        a0 += (s_mis[v * DV + k] & lbit) ? -m0 : m0;
+                    }
+                    const size_t w = (size_t)base + v;
+                    float* vr = S.vrow(w, lane);
+                    vr[32] = (float)a0 * iscale;
+                    reinterpret_cast<int*>(vr)[64] = a0;
+                    const unsigned n0 = __ballot_sync(kFull, (s_y[v] & lbit) ? a0 > 0 : a0 < 0);
+                    if (lane == 0) S.hard_w()[w] = n0;
+                }
+            } else {
+                for (int v = r; v < r + span; ++v) {
+                    const size_t w = (size_t)base + v;
+                    const unsigned yw = s_y[v];
+                    const unsigned y = (yw >> lane) & 1u;
+                    int a = Lf;
+#pragma unroll
+                    for (int k = 0; k < DV; ++k) {
+                        const unsigned mw = s_mis[v * DV + k];
+                        const int mf = s_mf[s_deg[v * DV + k] * 32 + lane];
+                        a += ((mw >> lane) & 1u) ? -mf : mf;
+                    }
+                    float* vr = S.vrow(w, lane);
+                    st_if(vr + 32, (float)a * iscale, live);
+                    if (live) reinterpret_cast<int*>(vr)[64] = a;   // acc = post'_1 in fixed point
+                    const unsigned neg = __ballot_sync(kFull, y ? a > 0 : a < 0);
+                    if (lane == 0) {
+                        const unsigned hw = (neg & act) | (yw & ~act);
+                        S.hard_w()[w] = hw;
+                        if (A.hist_w) A.hist_w[((size_t)1 * A.G) * A.n + w] = hw;
+                    }
                 }
             }
             __syncwarp();
