@@ -406,7 +406,7 @@ def main():
         "gpu_launches": 5 * args.steps,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": "mbp::decode_kernel (cooperative, all sweeps)",
+                     "kernel": "mbp::decode_scatter_kernel (cooperative, persistent, all sweeps)",
                      "kernel_ms": round(kms_mean, 4), "alg_bytes_per_launch": alg_bytes,
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                      "note": "achieved = SURVEY 8(d) message-streaming bytes / kernel time; the scatter "
