@@ -279,9 +279,10 @@ __device__ __forceinline__ void sc_row(const ScatterArgs& A, const SL<CPT>& S, c
         }
     }
     if (t >= kStoreFrom) {
-        // padded-ELL rows own Ds slots, so pad slots may be written
+        // only the row's own slots: the instance's degree bound D may exceed
+        // the ELL stride Ds (rounded-up instances, rows of degree < 3)
 #pragma unroll
-        for (int k = 0; k < DD; ++k) st_if(crow + k * 32, c[k], lv);
+        for (int k = 0; k < DD; ++k) st_if(crow + k * 32, c[k], lv && (!PAD || k < d));
     }
 #pragma unroll
     for (int k = 0; k < DD; ++k) {

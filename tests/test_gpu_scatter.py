@@ -181,3 +181,58 @@ def test_long_key_cfg4_against_oracle(cfg4_ensemble):
     assert np.array_equal(dec.syndromes(res.corrected), syn)
     frames = (0, 5)
     _assert_matches(res, _oracle_all(ens, fb.noisy, syn, 0.03, DecoderConfig(), frames), frames)
+
+
+def _random_ensemble(rng, u):
+    """u random irregular matrices sharing (n, m): column degrees 1-4, row
+    degrees whatever falls out (2..~30) -- exercises the padded / exact-degree
+    row variants, the wide-row instances and the irregular sweep-1 path."""
+    from paper_2001_07979_b200.matrix import MatrixEnsemble, ParityCheckMatrix
+
+    n = int(rng.integers(64, 1500))
+    m = int(rng.integers(max(8, n // 8), n // 2))
+    mats = []
+    while len(mats) < u:
+        rows = [[] for _ in range(m)]
+        for i in range(n):
+            for c in rng.choice(m, size=int(rng.integers(1, 5)), replace=False):
+                rows[int(c)].append(i)
+        if any(not r for r in rows):
+            continue
+        mats.append(ParityCheckMatrix.from_check_adjacency(n, m, rows))
+    return MatrixEnsemble(tuple(mats))
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_random_irregular_ensembles_against_oracle(seed):
+    rng = np.random.default_rng(1000 + seed)
+    ens = _random_ensemble(rng, int(rng.integers(1, 4)))
+    e = float(rng.uniform(0.01, 0.08))
+    clamp = float(rng.choice([8.0, 30.0, 45.0]))
+    B = int(rng.integers(33, 100))
+    cfg = DecoderConfig(max_iterations=int(rng.integers(5, 40)), llr_clamp=clamp)
+    fb = make_frames(ens.n, e, B, seed=seed)
+    dec = BatchDecoder(ens, B, cfg)
+    syn = dec.syndromes(fb.keys)
+    res = dec.decode(fb.noisy, syn, e)
+    _assert_matches(res, _oracle_all(ens, fb.noisy, syn, e, cfg))
+
+
+@pytest.mark.parametrize("variant", ["damping", "isolated", "fp64", "explicit"])
+@pytest.mark.parametrize("seed", range(4))
+def test_random_irregular_explicit_kernel_against_oracle(seed, variant):
+    """The explicit-message kernel (fp64 parity mode, damping, isolated
+    combining, MBP_EXPLICIT_MESSAGES) on the same random irregular ensembles."""
+    rng = np.random.default_rng(2000 + seed)
+    ens = _random_ensemble(rng, int(rng.integers(1, 4)))
+    e = float(rng.uniform(0.01, 0.07))
+    B = int(rng.integers(33, 70))
+    kw = {"damping": dict(damping=0.3), "isolated": dict(combining_mode="isolated-per-matrix"),
+          "fp64": dict(precision="fp64"), "explicit": {}}[variant]
+    cfg = DecoderConfig(max_iterations=int(rng.integers(5, 30)), **kw)
+    fb = make_frames(ens.n, e, B, seed=seed)
+    flags = N.MBP_EXPLICIT_MESSAGES if variant == "explicit" else 0
+    dec = BatchDecoder(ens, B, cfg, flags=flags)
+    syn = dec.syndromes(fb.keys)
+    res = dec.decode(fb.noisy, syn, e)
+    _assert_matches(res, _oracle_all(ens, fb.noisy, syn, e, cfg))
