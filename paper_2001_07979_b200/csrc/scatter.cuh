@@ -591,7 +591,7 @@ __device__ __forceinline__ void sc_var1_chunk(const ScatterArgs& A, const SL<CPT
 
 // sweep t >= 2: acc -> post'_t and the hard decision (acc is not re-armed:
 // the check phase adds message differences).
-template <bool CPT>
+template <bool CPT, int U>
 __device__ __forceinline__ void sc_var_chunk(const ScatterArgs& A, const SL<CPT>& S, int base, int end, int t,
                                              const int* cprev, int lane, unsigned* s_w, unsigned* s_old,
                                              float iscale)
@@ -612,7 +612,6 @@ __device__ __forceinline__ void sc_var_chunk(const ScatterArgs& A, const SL<CPT>
         const unsigned act = group_mask(cprev, g, lane);
         if (act) {
             const bool live = (act >> lane) & 1u;
-            constexpr int U = 8;   // independent acc loads in flight
             for (int k0 = 0; k0 < span; k0 += U) {
                 int a[U];
 #pragma unroll
@@ -865,7 +864,8 @@ __device__ __forceinline__ void sc_sweep(const ScatterArgs& A, int G, int t, int
         } else {
             const int ch = chunk_size(total, nwarps, 32);
             for (int base = claim(A.work + wc, lane, ch); base < total; base = claim(A.work + wc, lane, ch))
-                sc_var_chunk<CPT>(A, S, base, min(base + ch, total), t, cp, lane, s_w, s_x, iscale);
+                sc_var_chunk<CPT, (D <= 8 ? 16 : 32)>(A, S, base, min(base + ch, total), t, cp, lane, s_w, s_x,
+                                                      iscale);   // acc loads in flight: register budget
         }
         ++wc;
     }
