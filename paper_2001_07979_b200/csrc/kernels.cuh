@@ -210,7 +210,10 @@ template <> __device__ __forceinline__ float clampr<float>(float v, float c)
     return fminf(fmaxf(v, -c), c);
 }
 
-constexpr int kDecodeThreads = 256;  // decode kernel block size (decode.cuh)
+#ifndef MBP_DECODE_THREADS
+#define MBP_DECODE_THREADS 256
+#endif
+constexpr int kDecodeThreads = MBP_DECODE_THREADS;  // decode kernel block size (decode.cuh, scatter.cuh)
 
 // ---------------------------------------------------------------------------
 // bit-matrix transposes between BitBlock rows and 32-frame words
