@@ -172,6 +172,15 @@ int mbp_posterior_pass(mbp_ensemble *ens, int32_t precision, const double *c2v,
                        const double *priors, double *posterior);
 
 /* ---- pinned host memory for the host-buffer entry points ---------------- */
+/* ---- matrix construction (host) -----------------------------------------
+ * Progressive edge growth with the reference's tie-break stream
+ * (_kernels.peg_build, _kernels.py:57-161; matrix.peg_construct,
+ * matrix.py:215-234): the same seed gives the same matrix.  col_deg[n]
+ * column degrees; output rows chk_ptr[m+1], chk_var[sum(col_deg)] (sorted
+ * rows).  MBP_EUNSUPPORTED when no check can be attached.                  */
+int mbp_peg_build(int32_t n, int32_t m, const int32_t *col_deg, uint64_t seed, int64_t *chk_ptr,
+                  int32_t *chk_var);
+
 void *mbp_host_alloc(size_t bytes);
 void mbp_host_free(void *p);
 

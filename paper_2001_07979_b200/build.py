@@ -27,6 +27,7 @@ LIB = LIB_DIR / "libmbp_b200.so"
 # (object name, source, extra defines)
 UNITS = [
     ("mbp", "mbp.cu", []),
+    ("peg", "peg.cpp", []),
     ("k_explicit_f32", "k_explicit.cu", []),
     ("k_explicit_f64", "k_explicit.cu", ["-DMBP_EXPLICIT_F64=1"]),
     ("k_explicit_f64w", "k_explicit.cu", ["-DMBP_EXPLICIT_F64=2"]),
@@ -34,10 +35,11 @@ UNITS = [
     ("k_scatter_1", "k_scatter.cu", ["-DMBP_SCATTER_PART=1"]),
     ("k_scatter_2", "k_scatter.cu", ["-DMBP_SCATTER_PART=2"]),
 ]
-DEPS = sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [ROOT / "include" / "mbp.h"]
+DEPS = (sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + sorted(CSRC.glob("*.cpp"))
+        + [ROOT / "include" / "mbp.h"])
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-I", str(ROOT / "include")]
+NVCC_FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-I", str(ROOT / "include")]
 
 
 def nvcc() -> str:

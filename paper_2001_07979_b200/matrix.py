@@ -8,9 +8,10 @@ reference keeps doing so.
 
 Reference: ``ParityCheckMatrix`` / ``MatrixEnsemble`` (pkg/src/mmrecon/matrix.py:71-212),
 the stacked layout of ``DecoderWorkspace`` (pkg/src/mmrecon/decoder.py:80-122).
-PEG construction itself (matrix.py:215-260) is out of scope:
-ensembles ship as compact caches produced by the reference's ``build_ensemble``
-(``tests/golden/make_ensembles.py``).
+PEG construction (matrix.py:215-260) is restated exactly in
+the native library (``peg_construct`` / ``build_ensemble``, csrc/peg.cpp); the
+benchmark ensembles also ship as compact caches produced by the reference's
+``build_ensemble`` (``tests/golden/make_ensembles.py``).
 """
 
 from __future__ import annotations
@@ -32,6 +33,8 @@ __all__ = [
     "code_rate",
     "random_regular_matrix",
     "random_regular_ensemble",
+    "peg_construct",
+    "build_ensemble",
 ]
 
 ENSEMBLE_CACHE_VERSION = 1
@@ -165,6 +168,58 @@ class MatrixEnsemble:
 
     def content_hashes(self) -> list:
         return [h.content_hash() for h in self.matrices]
+
+
+def peg_construct(n: int, m: int, column_degree=3, seed: int = 0) -> ParityCheckMatrix:
+    """Progressive-edge-growth matrix, identical to the reference's
+    ``matrix.peg_construct(n, m, DegreeProfile, seed)`` (matrix.py:215-234)
+    for the same seed: ``mbp_peg_build`` in the native library restates
+    ``_kernels.peg_build`` (BFS order, candidate scan, xorshift64* ties).
+    ``column_degree``: an int (regular) or n per-column degrees (>= 2, as
+    DegreeProfile requires).  Sequential host code: seconds at n = 2^16,
+    hours at 2^20 (the reference's cost grows the same way, ~n*m)."""
+    import ctypes as C
+
+    from . import _native as N
+
+    if not 0 < m < n:
+        raise ValueError(f"need 0 < m < n, got m={m}, n={n}")
+    if np.ndim(column_degree) == 0:
+        if int(column_degree) < 2:
+            raise ValueError(f"column degree must be >= 2, got {column_degree}")
+        deg = np.full(n, int(column_degree), dtype=np.int32)
+    else:
+        deg = np.ascontiguousarray(column_degree, dtype=np.int32)
+        if deg.shape != (n,):
+            raise ValueError(f"profile lists {deg.size} degrees for n={n} columns")
+        if np.any(deg < 2):
+            raise ValueError("all column degrees must be >= 2")
+    if int(deg.max()) > m:
+        raise ValueError(f"column degree {int(deg.max())} exceeds m={m}: parallel edges would be forced")
+    E = int(deg.sum())
+    chk_ptr = np.zeros(m + 1, dtype=np.int64)
+    chk_var = np.zeros(E, dtype=np.int32)
+    N.call("mbp_peg_build", int(n), int(m), deg.ctypes.data, C.c_uint64(int(seed) & 0xFFFFFFFFFFFFFFFF),
+           chk_ptr.ctypes.data, chk_var.ctypes.data)
+    return ParityCheckMatrix._from_csr(n, m, chk_ptr, chk_var)
+
+
+def build_ensemble(n: int, m: int, column_degree=3, u: int = 1, base_seed: int = 0,
+                   workers: int | None = None) -> "MatrixEnsemble":
+    """u PEG matrices from seeds base_seed..base_seed+u-1, as the reference's
+    ``build_ensemble`` (matrix.py:237-256); members build in parallel
+    threads (the native call releases the GIL)."""
+    if u < 1:
+        raise ValueError(f"u must be >= 1, got {u}")
+    seeds = [base_seed + k for k in range(u)]
+    if u == 1 or (workers is not None and workers <= 1):
+        mats = [peg_construct(n, m, column_degree, s) for s in seeds]
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(max_workers=workers or min(u, 4)) as pool:
+            mats = list(pool.map(lambda s: peg_construct(n, m, column_degree, s), seeds))
+    return MatrixEnsemble(tuple(mats))
 
 
 def random_regular_matrix(n: int, m: int, dv: int = 3, seed: int = 0) -> ParityCheckMatrix:
