@@ -60,6 +60,11 @@
 namespace mbp {
 
 constexpr int kStoreFrom = 3;   // c2v_t is stored for t >= kStoreFrom
+
+#ifndef MBP_SPAN_UNROLL
+#define MBP_SPAN_UNROLL 2
+#endif
+constexpr int kSpanUnroll = MBP_SPAN_UNROLL;   // check-phase row loop unroll
 constexpr int kVB = 96;         // 32-bit words per variable block (3 lines)
 
 #ifndef MBP_SCATTER_MIN_BLOCKS
@@ -332,6 +337,11 @@ __device__ __forceinline__ void sc_span(const ScatterArgs& A, const SL<CPT>& S, 
         }
     }
     int dn = s_d[r0];
+    // two rows per loop pass for the narrow (64-register) instances: the
+    // prefetch buffers alternate instead of being copied; wide rows keep one
+    // (their 128-register budget is taken by the two-row chain prefetch)
+    constexpr int UR = D <= 8 ? kSpanUnroll : 1;
+#pragma unroll (UR)
     for (int r = r0; r < r1; ++r) {
         float p[D], p2[D];
 #pragma unroll
