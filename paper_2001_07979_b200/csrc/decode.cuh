@@ -365,7 +365,6 @@ template <int D> struct Chunk {
     static constexpr int CH = D <= 16 ? 32 : 8;   // items per claim (check / variable phases)
     static constexpr int SD = D | 1;               // odd smem row stride: conflict-free staging
 };
-constexpr int kSynChunk = 16;                      // syndrome-phase items (32 checks each)
 
 // items per claim: CH for large phases, fewer when a phase has less than
 // ~4 chunks per warp (small batches), so all warps get work

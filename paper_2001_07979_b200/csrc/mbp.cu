@@ -571,7 +571,7 @@ static int decode_chunk_scatter(mbp_workspace* ws, const uint8_t* noisy, const u
     A.cnt = ws->cnt.as<int>();
     A.Gb = G >= 2 ? std::min(ws->Gb, (G + 1) / 2) : 0;
     A.vb_b = ws->sc_vb_b.as<float>(); A.c2v_b = ws->c2v_b.as<float>();
-    A.Lmag_b = ws->Lmag_b.as<float>(); A.Mtab_b = ws->sc_Mtab_b.as<float>(); A.Lfix_b = ws->sc_Lfix_b.as<int>();
+    A.Mtab_b = ws->sc_Mtab_b.as<float>(); A.Lfix_b = ws->sc_Lfix_b.as<int>();
     A.noisy_b = ws->noisy_b.as<unsigned>(); A.syn_b = ws->syn_b.as<unsigned>(); A.mis_b = ws->sc_mis_b.as<unsigned>();
     A.hard_b = ws->hard_b.as<unsigned>(); A.cnt_b = ws->cnt_b.as<int>(); A.fid_b = ws->fid_b.as<int>();
     A.src_b = ws->src_b.as<int>(); A.newslot = ws->newslot.as<int>(); A.grp_cnt = ws->grp_cnt.as<int>();

@@ -104,7 +104,6 @@ struct ScatterArgs {
     int Gb;
     float* vb_b;
     float* c2v_b;
-    float* Lmag_b;
     float* Mtab_b;
     int* Lfix_b;
     unsigned* noisy_b;
@@ -802,7 +801,6 @@ __device__ __forceinline__ int sc_compact(const ScatterArgs& A, int t, int gw, i
     move_bits(A.mis_w, A.mis_b, A.C, Gn, A.src_b, gw, nw, lane);
     for (int s2 = gtid; s2 < Fb; s2 += nthreads) {
         const int s = ld_cg(A.src_b + s2);
-        A.Lmag_b[s2] = s >= 0 ? A.Lmag[s] : 0.0f;
         A.Lfix_b[s2] = s >= 0 ? ld_cg(A.Lfix + s) : 0;
         for (int d = 0; d <= A.Dm; ++d)
             A.Mtab_b[(size_t)d * A.Gb * 32 + s2] = s >= 0 ? A.Mtab[(size_t)d * A.G * 32 + s] : 0.0f;
