@@ -121,9 +121,14 @@ _DECODERS: dict = {}
 
 
 def _decoder_for(sub, cfg, batch, device):
-    key = (id(sub), cfg, batch, device)
+    """One device workspace per (matrix set, config, batch, device): grid
+    points of a sweep reuse it (``prefix(u)`` builds a new ensemble object
+    per call, so the key is the matrices' content hashes)."""
+    key = (tuple(sub.content_hashes()), cfg, batch, device)
     dec = _DECODERS.get(key)
     if dec is None:
+        if len(_DECODERS) >= 8:   # bound the device memory held by the cache
+            _DECODERS.pop(next(iter(_DECODERS)))
         dec = _DECODERS[key] = BatchDecoder(sub, batch, cfg, device=device)
     return dec
 

@@ -236,3 +236,35 @@ def test_random_irregular_explicit_kernel_against_oracle(seed, variant):
     syn = dec.syndromes(fb.keys)
     res = dec.decode(fb.noisy, syn, e)
     _assert_matches(res, _oracle_all(ens, fb.noisy, syn, e, cfg))
+
+
+@pytest.mark.parametrize("e", [0.004, 0.012])
+def test_low_qber_early_compaction(cfg1_ensemble, e):
+    """At low QBER most frames stop after iteration 0 or sweep 1, so frames
+    are compacted at the start of sweep 2 (the rebuilt-base path in the
+    compacted layout, absolute accumulation); outputs equal the uncompacted
+    decode and the oracle."""
+    fb = make_frames(cfg1_ensemble.n, e, 256, seed=101)
+    on = BatchDecoder(cfg1_ensemble, 256)
+    off = BatchDecoder(cfg1_ensemble, 256, flags=N.MBP_NO_COMPACTION)
+    syn = on.syndromes(fb.keys)
+    a = on.decode(fb.noisy, syn, e)
+    b = off.decode(fb.noisy, syn, e)
+    for f in ("corrected", "converged", "iterations", "mismatches"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
+    assert on.last_stats()[1] in (0, 2, 3)
+    frames = list(range(0, 256, 16))
+    _assert_matches(a, _oracle_all(cfg1_ensemble, fb.noisy, syn, e, DecoderConfig(), frames), frames)
+
+
+@pytest.mark.parametrize("e", [1e-12, 0.45])
+def test_extreme_crossover_probabilities(cfg1_ensemble, e):
+    """Huge priors (e -> 0: the fixed-point scale shrinks) and near-zero
+    priors (e -> 0.5: decoding fails to the limit) against the oracle."""
+    cfg = DecoderConfig(max_iterations=12)
+    fb = make_frames(cfg1_ensemble.n, min(e, 0.02), 40, seed=111)
+    dec = BatchDecoder(cfg1_ensemble, 40, cfg)
+    syn = dec.syndromes(fb.keys)
+    res = dec.decode(fb.noisy, syn, e)
+    frames = list(range(0, 40, 5))
+    _assert_matches(res, _oracle_all(cfg1_ensemble, fb.noisy, syn, e, cfg, frames), frames)
