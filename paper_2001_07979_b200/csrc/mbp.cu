@@ -47,6 +47,15 @@ float saturation_threshold()
     return f;
 }
 
+}  // namespace
+
+// error reporting for the host-only translation units (peg.cpp)
+namespace mbp {
+int set_error(int code, const char* msg) { return fail(code, msg); }
+}  // namespace mbp
+
+namespace {
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;

@@ -18,6 +18,10 @@
 #include <cstdint>
 #include <vector>
 
+namespace mbp {
+int set_error(int code, const char* msg);   // mbp.cu: thread-local mbp_last_error()
+}
+
 namespace {
 
 inline uint64_t splitmix64(uint64_t x)
@@ -58,12 +62,12 @@ struct DegreeSets {
 
 int mbp_peg_build(int32_t n, int32_t m, const int32_t* col_deg, uint64_t seed, int64_t* chk_ptr, int32_t* chk_var)
 {
-    if (!col_deg || !chk_ptr || !chk_var) return MBP_EINVAL;
-    if (!(0 < m && m < n)) return MBP_EINVAL;
+    if (!col_deg || !chk_ptr || !chk_var) return mbp::set_error(MBP_EINVAL, "null pointer argument");
+    if (!(0 < m && m < n)) return mbp::set_error(MBP_EINVAL, "need 0 < m < n");
     int64_t E = 0;
     int dmax = 0;
     for (int i = 0; i < n; ++i) {
-        if (col_deg[i] < 1 || col_deg[i] > m) return MBP_EINVAL;
+        if (col_deg[i] < 1 || col_deg[i] > m) return mbp::set_error(MBP_EINVAL, "column degree outside [1, m]");
         E += col_deg[i];
         dmax = col_deg[i] > dmax ? col_deg[i] : dmax;
     }
@@ -184,7 +188,7 @@ int mbp_peg_build(int32_t n, int32_t m, const int32_t* col_deg, uint64_t seed, i
                 }
             }
             for (int c : reached_list) reached_bits[c >> 6] &= ~(1ull << (c & 63));
-            if (best < 0) return MBP_EUNSUPPORTED;   // no attachable check (infeasible request)
+            if (best < 0) return mbp::set_error(MBP_EUNSUPPORTED, "PEG found no attachable check node");
             ds.remove(best, cn_deg[best]);
             ++cn_deg[best];
             ds.add(best, cn_deg[best]);
@@ -199,5 +203,5 @@ int mbp_peg_build(int32_t n, int32_t m, const int32_t* col_deg, uint64_t seed, i
         int64_t o = chk_ptr[c];
         for (int w : cn_adj[c]) chk_var[o++] = w;
     }
-    return chk_ptr[m] == E ? MBP_OK : MBP_ECUDA;
+    return chk_ptr[m] == E ? MBP_OK : mbp::set_error(MBP_EINVAL, "internal: edge count mismatch");
 }
