@@ -226,9 +226,12 @@ __device__ __forceinline__ void rule_sd(const float (&x)[DD], int d, unsigned fl
 // chain c2v'_s = rule(clamp(post'_{s-1} - c2v'_{s-1})), s = s0..t, ends in
 // c2v'_t, which is added into acc (and stored when t >= kStoreFrom).  The
 // first gather (post'_{s0-1}) of the next row is issued before the current
-// row's rule (software pipeline).  FULL: every lane of the group is live.
+// row's rule (software pipeline).  Dead lanes (converged frames, empty
+// slots) run the same unpredicated gathers and rules (every word they read
+// is allocated, every rule output finite: min(|x|, clamp) drops NaN) and
+// are masked by their zero `scale`: their acc deltas round to 0.
 // ---------------------------------------------------------------------------
-template <int D, int DD, bool PAD, bool FULL, bool SAT, bool T2, bool CPT, bool C3 = false>
+template <int D, int DD, bool PAD, bool SAT, bool T2, bool CPT, bool C3 = false>
 __device__ __forceinline__ void sc_row(const ScatterArgs& A, const SL<CPT>& S, const float (&p)[D], int d,
                                        unsigned sj, float M1, const unsigned* soff, bool live, int t_,
                                        const float* gb, const float* qrow, float* crow, float scale, bool absolute,
@@ -237,7 +240,6 @@ __device__ __forceinline__ void sc_row(const ScatterArgs& A, const SL<CPT>& S, c
     // C3: sweep 3 with the rebuilt chain, post'_2 values prefetched by the caller
     // T2: sweep 2, the hot case (no chain, no store) compiled on its own
     const int t = T2 ? 2 : t_;
-    const bool lv = FULL || live;
     const bool explicit_base = !T2 && t > kStoreFrom;
     float c[DD];
     if (!explicit_base) {
@@ -246,7 +248,7 @@ __device__ __forceinline__ void sc_row(const ScatterArgs& A, const SL<CPT>& S, c
         for (int k = 0; k < DD; ++k) c[k] = c1;
     } else {
 #pragma unroll
-        for (int k = 0; k < DD; ++k) c[k] = ld_cg_if(qrow + k * 32, lv && (!PAD || k < d));
+        for (int k = 0; k < DD; ++k) c[k] = ld_cg_if(qrow + k * 32, live && (!PAD || k < d));   // 0 when dead
     }
     float x[DD];
 #pragma unroll
@@ -274,7 +276,7 @@ __device__ __forceinline__ void sc_row(const ScatterArgs& A, const SL<CPT>& S, c
                     pv = p2[k];
                 } else {
                     const float* q = byte_off(gs, soff[k]);
-                    pv = FULL ? ld_cg(q) : ld_cg_if(q, live);
+                    pv = ld_cg(q);
                 }
                 x[k] = pv - c[k];
                 if (s == t) vold[k] = __float2int_rn(c[k] * scale);
@@ -286,12 +288,12 @@ __device__ __forceinline__ void sc_row(const ScatterArgs& A, const SL<CPT>& S, c
         // only the row's own slots: the instance's degree bound D may exceed
         // the ELL stride Ds (rounded-up instances, rows of degree < 3)
 #pragma unroll
-        for (int k = 0; k < DD; ++k) st_if(crow + k * 32, c[k], lv && (!PAD || k < d));
+        for (int k = 0; k < DD; ++k) st_if(crow + k * 32, c[k], !PAD || k < d);
     }
 #pragma unroll
     for (int k = 0; k < DD; ++k) {
         const int v = __float2int_rn(c[k] * scale) - (CPT && absolute ? 0 : vold[k]);
-        red_add(byte_off(gb, soff[k]) + 64, (lv && (!PAD || k < d)) ? v : 0);   // acc line
+        red_add(byte_off(gb, soff[k]) + 64, (!PAD || k < d) ? v : 0);   // acc line
     }
 }
 
@@ -310,7 +312,7 @@ __device__ __forceinline__ const float* sc_c2v_in_base(const ScatterArgs& A, con
 }
 
 // rows [r0, r1) of the staged chunk, all in group g (first row j0)
-template <int D, bool FULL, bool SAT, bool T2, bool CPT, bool C3 = false>
+template <int D, bool SAT, bool T2, bool CPT, bool C3 = false>
 __device__ __forceinline__ void sc_span(const ScatterArgs& A, const SL<CPT>& S, int g, int j0, int r0, int r1, int t,
                                         unsigned act, int lane, const unsigned* s_off, const unsigned* s_m,
                                         const int* s_d, const float* s_m1, bool first, float scale)
@@ -319,6 +321,7 @@ __device__ __forceinline__ void sc_span(const ScatterArgs& A, const SL<CPT>& S, 
     if (T2) t = 2;
     if (C3) t = 3;
     const bool live = (act >> lane) & 1u;
+    scale = live ? scale : 0.0f;
     const bool explicit_base = !T2 && t > kStoreFrom;
     const float* gb = S.vrow((size_t)g * A.n, lane);
     const float* qb = explicit_base ? sc_c2v_in_base<CPT>(A, S, g, lane, first) : nullptr;
@@ -329,10 +332,10 @@ __device__ __forceinline__ void sc_span(const ScatterArgs& A, const SL<CPT>& S, 
 #pragma unroll
     for (int k = 0; k < D; ++k) {
         const float* q = byte_off(gf, s_off[r0 * SD + k]);
-        pn[k] = FULL ? ld_cg(q) : ld_cg_if(q, live);
+        pn[k] = ld_cg(q);
         if constexpr (C3) {
             const float* q2 = byte_off(g2, s_off[r0 * SD + k]);
-            pn2[k] = FULL ? ld_cg(q2) : ld_cg_if(q2, live);
+            pn2[k] = ld_cg(q2);
         }
     }
     int dn = s_d[r0];
@@ -354,10 +357,10 @@ __device__ __forceinline__ void sc_span(const ScatterArgs& A, const SL<CPT>& S, 
 #pragma unroll
             for (int k = 0; k < D; ++k) {
                 const float* q = byte_off(gf, s_off[(r + 1) * SD + k]);
-                pn[k] = FULL ? ld_cg(q) : ld_cg_if(q, live);
+                pn[k] = ld_cg(q);
                 if constexpr (C3) {
                     const float* q2 = byte_off(g2, s_off[(r + 1) * SD + k]);
-                    pn2[k] = FULL ? ld_cg(q2) : ld_cg_if(q2, live);
+                    pn2[k] = ld_cg(q2);
                 }
             }
         }
@@ -372,13 +375,13 @@ __device__ __forceinline__ void sc_span(const ScatterArgs& A, const SL<CPT>& S, 
         const float* qrow = explicit_base ? qb + (size_t)j * A.Ds * 32 : nullptr;
         float* crow = t >= kStoreFrom ? S.c2v() + ((size_t)g * A.slots + (size_t)j * A.Ds) * 32 + lane : nullptr;
         if (d == D)
-            sc_row<D, D, false, FULL, SAT, T2, CPT, C3>(A, S, p, d, sj, M1, soff, live, t, gb, qrow, crow, scale,
+            sc_row<D, D, false, SAT, T2, CPT, C3>(A, S, p, d, sj, M1, soff, live, t, gb, qrow, crow, scale,
                                                         first, p2);
         else if (D > 1 && d == D - 1)
-            sc_row<D, (D > 1 ? D - 1 : 1), false, FULL, SAT, T2, CPT, C3>(A, S, p, d, sj, M1, soff, live, t, gb,
+            sc_row<D, (D > 1 ? D - 1 : 1), false, SAT, T2, CPT, C3>(A, S, p, d, sj, M1, soff, live, t, gb,
                                                                           qrow, crow, scale, first, p2);
         else
-            sc_row<D, D, true, FULL, SAT, T2, CPT, C3>(A, S, p, d, sj, M1, soff, live, t, gb, qrow, crow, scale,
+            sc_row<D, D, true, SAT, T2, CPT, C3>(A, S, p, d, sj, M1, soff, live, t, gb, qrow, crow, scale,
                                                        first, p2);
     }
 }
@@ -416,21 +419,21 @@ __device__ __forceinline__ void sc_check_chunk(const ScatterArgs& A, const SL<CP
                     __syncwarp();
                 }
             }
-            // fast variants: every lane live and no input can saturate, sweep
-            // 2 (the hot case) compiled on its own
-            if (act == kFull && A.clamp < A.sat) {
+            // fast variants: no input can saturate; sweeps 2 and 3 (the hot
+            // cases) compiled on their own
+            if (A.clamp < A.sat) {
                 if (t == 2)
-                    sc_span<D, true, false, true, CPT>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d, s_m1,
-                                                       first, scale);
+                    sc_span<D, false, true, CPT>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d, s_m1, first,
+                                                 scale);
                 else if (t == 3 && kStoreFrom == 3)
-                    sc_span<D, true, false, false, CPT, true>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d,
-                                                              s_m1, first, scale);
+                    sc_span<D, false, false, CPT, true>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d, s_m1,
+                                                        first, scale);
                 else
-                    sc_span<D, true, false, false, CPT>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d,
-                                                        s_m1, first, scale);
+                    sc_span<D, false, false, CPT>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d, s_m1, first,
+                                                  scale);
             } else {
-                sc_span<D, false, true, false, CPT>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d, s_m1,
-                                                    first, scale);
+                sc_span<D, true, false, CPT>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d, s_m1, first,
+                                             scale);
             }
             __syncwarp();
         }

@@ -54,7 +54,8 @@ def main():
     it = out[2].cpu().numpy()
     ok = out[1].cpu().numpy().astype(bool) & np.all(out[0].cpu().numpy() == fb.keys, axis=1)
     print(json.dumps({"cfg": a.cfg, "frames": a.frames, "e": a.e, "precision": a.precision,
-                      "mean_iterations": float(it.mean()), "good": int(ok.sum()), "runs": res}, indent=1))
+                      "mean_iterations": float(it.mean()),
+                      "iteration_histogram": {int(k): int(v) for k, v in zip(*np.unique(it, return_counts=True))}, "good": int(ok.sum()), "runs": res}, indent=1))
 
 
 if __name__ == "__main__":
