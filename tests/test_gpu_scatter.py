@@ -268,3 +268,18 @@ def test_extreme_crossover_probabilities(cfg1_ensemble, e):
     res = dec.decode(fb.noisy, syn, e)
     frames = list(range(0, 40, 5))
     _assert_matches(res, _oracle_all(cfg1_ensemble, fb.noisy, syn, e, cfg, frames), frames)
+
+
+def test_partially_live_groups_sweeps_2_3(cfg2_ensemble):
+    """cfg 2 at e = 0.04: a few frames of each 32-frame group finish after
+    sweep 2, the rest after sweep 3, so the sweep-3 check phase runs its fast
+    path on partially live groups (dead lanes masked by a zero fixed-point
+    scale, scatter.cuh sc_span); the finished frames' outputs must not move."""
+    B = 64
+    fb = make_frames(cfg2_ensemble.n, 0.04, B, seed=0)
+    dec = BatchDecoder(cfg2_ensemble, B, flags=N.MBP_NO_COMPACTION)
+    syn = dec.syndromes(fb.keys)
+    res = dec.decode(fb.noisy, syn, 0.04)
+    it = res.iterations.reshape(2, 32)
+    assert any(set(row.tolist()) >= {2, 3} for row in it), it
+    _assert_matches(res, _oracle_all(cfg2_ensemble, fb.noisy, syn, 0.04, DecoderConfig()))
