@@ -395,7 +395,8 @@ def main():
         "warmup": args.warmup, "ms_per_step": round(total_ms_max / args.steps, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32" if args.precision == "fp32" else "f64",
-        "data": "synthetic (reference Philox frame streams, PEG ensemble from the reference)",
+        "data": "synthetic (reference Philox frame streams, "
+                + ("synthetic random regular graphs)" if args.workload == "cfg4" else "PEG ensemble from the reference)"),
         "config": config_dict(args, ens),
         "fer": round(1.0 - float(conv.mean()), 6), "mean_iterations": round(float(iters.mean()), 4),
         "sweeps_run": sweeps,
