@@ -309,6 +309,11 @@ class BatchDecoder:
         if cts[0] > 0:
             cd = np.diff(cts)
             out["compaction_ms"] = {"maps": float(cd[0]), "move": float(cd[1]), "barrier": float(cd[2])}
+            # the compaction runs between a sweep's first stamp and its check
+            # phase: report that check phase without it
+            for i in range(sweeps):
+                if ts[1 + 3 * i] <= cts[0] <= ts[2 + 3 * i]:
+                    out["check_ms"][i] -= float(cts[3] - cts[0])
         return out
 
     def last_stats(self):
