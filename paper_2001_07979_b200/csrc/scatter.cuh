@@ -770,7 +770,10 @@ __device__ __forceinline__ int sc_compact(const ScatterArgs& A, int t, int gw, i
     {
         const bool both = t <= kStoreFrom;
         const int keep = ((t - 1) & 1) * 32;
-        constexpr int XU = 8;
+#ifndef MBP_MOVE_XU
+#define MBP_MOVE_XU 4
+#endif
+        constexpr int XU = MBP_MOVE_XU;   // variables per lane and pass (gathers in flight)
         const long long xchunks = (A.n + XU - 1) / XU;
         for (long long it = gw; it < (long long)Gn * xchunks; it += nw) {
             const int g2 = (int)(it / xchunks);
