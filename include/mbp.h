@@ -171,7 +171,6 @@ int mbp_v2c_pass(mbp_ensemble *ens, int32_t precision, int32_t matrix_index, int
 int mbp_posterior_pass(mbp_ensemble *ens, int32_t precision, const double *c2v,
                        const double *priors, double *posterior);
 
-/* ---- pinned host memory for the host-buffer entry points ---------------- */
 /* ---- matrix construction (host) -----------------------------------------
  * Progressive edge growth with the reference's tie-break stream
  * (_kernels.peg_build, _kernels.py:57-161; matrix.peg_construct,
@@ -181,6 +180,7 @@ int mbp_posterior_pass(mbp_ensemble *ens, int32_t precision, const double *c2v,
 int mbp_peg_build(int32_t n, int32_t m, const int32_t *col_deg, uint64_t seed, int64_t *chk_ptr,
                   int32_t *chk_var);
 
+/* ---- pinned host memory for the host-buffer entry points ---------------- */
 void *mbp_host_alloc(size_t bytes);
 void mbp_host_free(void *p);
 
