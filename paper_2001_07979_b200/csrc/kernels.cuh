@@ -254,23 +254,39 @@ static __global__ void __launch_bounds__(256) rows_to_words_kernel(
     const int tiles = (int)((seg_bytes + kTileBytes - 1) / kTileBytes);
     const long long total = (long long)G * nseg * tiles;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // 16-byte row accesses when every row segment is 16-byte aligned
+    const bool vec = row_bytes % 16 == 0 && seg_bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(rows) & 15) == 0;
     for (long long it = blockIdx.x; it < total; it += gridDim.x) {
         const int xt = (int)(it % tiles);
         const int s = (int)((it / tiles) % nseg);
         const int g = (int)(it / ((long long)tiles * nseg));
         const long long b0 = (long long)xt * kTileBytes;
-        uint8_t v[32 * kTileBytes / 256];   // all loads in flight before the stores
-#pragma unroll
-        for (int q = 0; q < 32 * kTileBytes / 256; ++q) {
-            const int idx = threadIdx.x + 256 * q;
-            const int r = idx / kTileBytes, b = idx % kTileBytes;
+        if (vec) {
+            // one 16-byte load per thread: row r = tid / 8, bytes 16 (tid % 8)
+            const int r = threadIdx.x >> 3, b = (threadIdx.x & 7) * 16;
             const int f = g * 32 + r;
-            v[q] = (f < B && b0 + b < seg_bytes) ? rows[(long long)f * row_bytes + (long long)s * seg_bytes + b0 + b] : 0;
-        }
+            uint4 x = make_uint4(0u, 0u, 0u, 0u);
+            if (f < B && b0 + b < seg_bytes)
+                x = __ldg(reinterpret_cast<const uint4*>(rows + (long long)f * row_bytes + (long long)s * seg_bytes + b0 + b));
+            unsigned* t = reinterpret_cast<unsigned*>(tile + r * kTileStride + b);
+            t[0] = x.x;
+            t[1] = x.y;
+            t[2] = x.z;
+            t[3] = x.w;
+        } else {
+            uint8_t v[32 * kTileBytes / 256];   // all loads in flight before the stores
 #pragma unroll
-        for (int q = 0; q < 32 * kTileBytes / 256; ++q) {
-            const int idx = threadIdx.x + 256 * q;
-            tile[(idx / kTileBytes) * kTileStride + idx % kTileBytes] = v[q];
+            for (int q = 0; q < 32 * kTileBytes / 256; ++q) {
+                const int idx = threadIdx.x + 256 * q;
+                const int r = idx / kTileBytes, b = idx % kTileBytes;
+                const int f = g * 32 + r;
+                v[q] = (f < B && b0 + b < seg_bytes) ? rows[(long long)f * row_bytes + (long long)s * seg_bytes + b0 + b] : 0;
+            }
+#pragma unroll
+            for (int q = 0; q < 32 * kTileBytes / 256; ++q) {
+                const int idx = threadIdx.x + 256 * q;
+                tile[(idx / kTileBytes) * kTileStride + idx % kTileBytes] = v[q];
+            }
         }
         __syncthreads();
 #pragma unroll
@@ -299,6 +315,8 @@ static __global__ void __launch_bounds__(256) words_to_rows_kernel(
     const int tiles = (int)((seg_bytes + kTileBytes - 1) / kTileBytes);
     const long long total = (long long)G * nseg * tiles;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // 16-byte row accesses when every row segment is 16-byte aligned
+    const bool vec = row_bytes % 16 == 0 && seg_bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(rows) & 15) == 0;
     for (long long it = blockIdx.x; it < total; it += gridDim.x) {
         const int xt = (int)(it % tiles);
         const int s = (int)((it / tiles) % nseg);
@@ -312,13 +330,23 @@ static __global__ void __launch_bounds__(256) words_to_rows_kernel(
             *reinterpret_cast<unsigned*>(tile + lane * kTileStride + 4 * c) = warp_transpose32(w, lane);
         }
         __syncthreads();
-#pragma unroll
-        for (int q = 0; q < 32 * kTileBytes / 256; ++q) {
-            const int idx = threadIdx.x + 256 * q;
-            const int r = idx / kTileBytes, b = idx % kTileBytes;
+        if (vec) {
+            const int r = threadIdx.x >> 3, b = (threadIdx.x & 7) * 16;
             const int f = g * 32 + r;
-            if (f < B && b0 + b < seg_bytes)
-                rows[(long long)f * row_bytes + (long long)s * seg_bytes + b0 + b] = tile[r * kTileStride + b];
+            if (f < B && b0 + b < seg_bytes) {
+                const unsigned* t = reinterpret_cast<const unsigned*>(tile + r * kTileStride + b);
+                *reinterpret_cast<uint4*>(rows + (long long)f * row_bytes + (long long)s * seg_bytes + b0 + b) =
+                    make_uint4(t[0], t[1], t[2], t[3]);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 32 * kTileBytes / 256; ++q) {
+                const int idx = threadIdx.x + 256 * q;
+                const int r = idx / kTileBytes, b = idx % kTileBytes;
+                const int f = g * 32 + r;
+                if (f < B && b0 + b < seg_bytes)
+                    rows[(long long)f * row_bytes + (long long)s * seg_bytes + b0 + b] = tile[r * kTileStride + b];
+            }
         }
         __syncthreads();
     }
