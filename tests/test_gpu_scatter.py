@@ -283,3 +283,27 @@ def test_partially_live_groups_sweeps_2_3(cfg2_ensemble):
     it = res.iterations.reshape(2, 32)
     assert any(set(row.tolist()) >= {2, 3} for row in it), it
     _assert_matches(res, _oracle_all(cfg2_ensemble, fb.noisy, syn, 0.04, DecoderConfig()))
+
+
+def test_phase_timers_account_for_the_compaction(cfg2_ensemble):
+    """MBP_PROFILE_PHASES stamps: with a compaction the phases (initial check,
+    per-sweep check / variable / syndrome, compaction, tail) add up to the
+    kernel's stamped span, and decisions are those of the unprofiled decode."""
+    import torch
+
+    B = 256
+    fb = make_frames(cfg2_ensemble.n, 0.03, B, seed=5)
+    dev = torch.device("cuda:0")
+    dec = BatchDecoder(cfg2_ensemble, B, flags=N.MBP_PROFILE_PHASES)
+    syn = dec.syndromes(torch.from_numpy(fb.keys).to(dev))
+    out = dec.decode_device(torch.from_numpy(fb.noisy).to(dev), syn, 0.03)
+    torch.cuda.synchronize()
+    pt = dec.phase_times()
+    assert dec.last_stats()[1] >= 2 and "compaction_ms" in pt, pt
+    parts = (pt["syncheck0_ms"] + sum(pt["check_ms"]) + sum(pt["var_ms"]) + sum(pt["syncheck_ms"])
+             + sum(pt["compaction_ms"].values()) + pt["tail_ms"])
+    assert min(pt["check_ms"]) >= 0.0
+    assert abs(parts - pt["total_ms"]) <= 0.02 * pt["total_ms"] + 1e-3, (parts, pt)
+    ref = BatchDecoder(cfg2_ensemble, B).decode_device(torch.from_numpy(fb.noisy).to(dev), syn, 0.03)
+    for a, b in zip(out, ref):
+        assert torch.equal(a, b)
