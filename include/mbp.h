@@ -146,8 +146,9 @@ int mbp_decode_batch(mbp_workspace *ws, const uint8_t *noisy, const uint8_t *syn
  * Frame indices are relative to the last (single-chunk) batch.             */
 int mbp_workspace_read_posterior(mbp_workspace *ws, int64_t frame, double *posterior_n);
 int mbp_workspace_read_c2v(mbp_workspace *ws, int64_t frame, double *c2v_E);
-/* v2c as last formed by the check phase (damping only): the message the
- * final sweep's C2V consumed, i.e. the previous v2c of the last v2c_pass. */
+/* v2c as last formed by the check phase (damping with MBP_KEEP_STATE only):
+ * the message the final sweep's C2V consumed, i.e. the previous v2c of the
+ * last v2c_pass.                                                           */
 int mbp_workspace_read_v2c(mbp_workspace *ws, int64_t frame, double *v2c_E);
 /* rows [0, rows) of frame's decision history, packed [rows][ceil(n/8)] */
 int mbp_workspace_read_history(mbp_workspace *ws, int64_t frame, int32_t rows, uint8_t *out);
@@ -162,7 +163,8 @@ int mbp_workspace_read_phase_times(mbp_workspace *ws, uint64_t *ns, int32_t cap,
 /* ---- single phases on explicit per-edge messages of ONE frame ------------
  * (decoder.py:155-200).  Host arrays in the reference's float64 layout:
  * v2c/c2v [E], priors/posterior [n]; syn_bits u8[m] of the given matrix.
- * Computed with the device kernels in the given precision.                 */
+ * Computed with the device kernels in the given precision, on a stream of
+ * the ensemble's own (not the legacy default stream); synchronous.         */
 int mbp_c2v_pass(mbp_ensemble *ens, int32_t precision, int32_t matrix_index,
                  const uint8_t *syn_bits, double clamp, const double *v2c, double *c2v);
 int mbp_v2c_pass(mbp_ensemble *ens, int32_t precision, int32_t matrix_index, int32_t joint,
@@ -179,6 +181,23 @@ int mbp_posterior_pass(mbp_ensemble *ens, int32_t precision, const double *c2v,
  * rows).  MBP_EUNSUPPORTED when no check can be attached.                  */
 int mbp_peg_build(int32_t n, int32_t m, const int32_t *col_deg, uint64_t seed, int64_t *chk_ptr,
                   int32_t *chk_var);
+
+/* ---- synthetic BSC frames (the reference's frame streams) ---------------
+ * Rows [batch][ceil(n/8)] of Alice's keys and Bob's noisy keys for frames
+ * first .. first+batch-1 of a grid point, bit-identical to the reference's
+ * bench._frame_inputs (bench.py:123-130) / channel.rng_stream
+ * (channel.py:29-35): frame idx's key is
+ *   Philox(SeedSequence((seed, *path, idx, 0))).integers(0, 2, n, uint8)
+ * and its flips Philox(SeedSequence((seed, *path, idx, 1))).random(n) < e.
+ * prefix: the SeedSequence entropy words of (seed, *path) -- each integer
+ * as its little-endian uint32 words, 0 as one zero word (numpy's
+ * _coerce_to_uint32_array) -- at most 21 words.  _device: rows in device
+ * memory, enqueued on `stream`.  Host variant: the same code on `threads`
+ * host threads (no GPU needed).                                             */
+int mbp_frames_generate_device(int32_t n, const uint32_t *prefix, int32_t prefix_len, int64_t first,
+                               int64_t batch, double e, uint8_t *keys, uint8_t *noisy, void *stream);
+int mbp_frames_generate(int32_t n, const uint32_t *prefix, int32_t prefix_len, int64_t first,
+                        int64_t batch, double e, uint8_t *keys, uint8_t *noisy, int32_t threads);
 
 /* ---- pinned host memory for the host-buffer entry points ---------------- */
 void *mbp_host_alloc(size_t bytes);

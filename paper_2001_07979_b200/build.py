@@ -28,6 +28,7 @@ LIB = LIB_DIR / "libmbp_b200.so"
 UNITS = [
     ("mbp", "mbp.cu", []),
     ("peg", "peg.cpp", []),
+    ("frames", "frames.cu", []),
     ("k_explicit_f32", "k_explicit.cu", []),
     ("k_explicit_f64", "k_explicit.cu", ["-DMBP_EXPLICIT_F64=1"]),
     ("k_explicit_f64w", "k_explicit.cu", ["-DMBP_EXPLICIT_F64=2"]),

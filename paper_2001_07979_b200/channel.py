@@ -16,7 +16,7 @@ import numpy as np
 from .bits import BitBlock
 
 __all__ = ["rng_stream", "binary_entropy", "efficiency", "generate_key", "frame_bits",
-           "FrameBatch", "make_frames"]
+           "FrameBatch", "make_frames", "entropy_words", "make_frames_native", "make_frames_device"]
 
 
 def rng_stream(seed: int, *path: int) -> np.random.Generator:
@@ -81,6 +81,72 @@ def make_frames(n: int, e: float, frames: int, seed: int = 0, path: tuple = (),
         keys[k] = np.packbits(kb, bitorder="little")
         noisy[k] = np.packbits(yb, bitorder="little")
     return FrameBatch(keys, noisy, n, e)
+
+
+def entropy_words(*ints: int) -> np.ndarray:
+    """SeedSequence entropy words of a tuple of non-negative ints (numpy's
+    _coerce_to_uint32_array: little-endian uint32 words, 0 -> one zero word)."""
+    words = []
+    for x in ints:
+        x = int(x)
+        if x < 0:
+            raise ValueError("expected non-negative integers")
+        if x == 0:
+            words.append(0)
+        while x:
+            words.append(x & 0xFFFFFFFF)
+            x >>= 32
+    return np.asarray(words, dtype=np.uint32)
+
+
+def _frame_prefix(seed: int, path: tuple) -> np.ndarray:
+    w = entropy_words(seed, *path)
+    if w.size > 21:
+        raise ValueError("seed + path exceed 21 entropy words")
+    return np.ascontiguousarray(w)
+
+
+def make_frames_native(n: int, e: float, frames: int, seed: int = 0, path: tuple = (),
+                       start: int = 0, threads: int | None = None) -> FrameBatch:
+    """make_frames through the library's generator on host threads
+    (mbp_frames_generate; frames.cuh restates numpy's SeedSequence / Philox /
+    integers / random, checked bit for bit against make_frames in tests)."""
+    import os
+
+    from . import _native as N
+
+    nb = (n + 7) // 8
+    keys = np.empty((frames, nb), dtype=np.uint8)
+    noisy = np.empty((frames, nb), dtype=np.uint8)
+    pre = _frame_prefix(seed, tuple(path))
+    N.call("mbp_frames_generate", int(n), pre.ctypes.data, int(pre.size), int(start), int(frames), float(e),
+           keys.ctypes.data, noisy.ctypes.data, int(threads or os.cpu_count() or 1))
+    return FrameBatch(keys, noisy, n, e)
+
+
+def make_frames_device(n: int, e: float, frames: int, seed: int = 0, path: tuple = (), start: int = 0,
+                       device: int = 0, out=None, stream=None):
+    """The same frames generated in HBM (mbp_frames_generate_device): returns
+    (keys, noisy) uint8 CUDA tensors [frames, ceil(n/8)] on ``device``,
+    enqueued on the current torch stream (or ``stream``)."""
+    import ctypes as C
+
+    import torch
+
+    from . import _native as N
+
+    nb = (n + 7) // 8
+    dev = torch.device("cuda", device)
+    keys, noisy = out if out is not None else (torch.empty((frames, nb), dtype=torch.uint8, device=dev),
+                                               torch.empty((frames, nb), dtype=torch.uint8, device=dev))
+    for t in (keys, noisy):
+        if t.dtype != torch.uint8 or not t.is_cuda or not t.is_contiguous() or tuple(t.shape) != (frames, nb):
+            raise ValueError(f"output rows must be contiguous uint8 CUDA tensors of shape {(frames, nb)}")
+    pre = _frame_prefix(seed, tuple(path))
+    s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    N.call("mbp_frames_generate_device", int(n), pre.ctypes.data, int(pre.size), int(start), int(frames),
+           float(e), keys.data_ptr(), noisy.data_ptr(), C.c_void_p(s))
+    return keys, noisy
 
 
 def bsc_flips(n: int, e: float, seed: int) -> np.ndarray:

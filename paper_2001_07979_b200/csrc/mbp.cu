@@ -106,6 +106,10 @@ struct mbp_ensemble {
     // decode layout: padded ELL rows + slot ids per variable
     DevBuf deg, chk_ell, var_slot, ref2slot;
     DevBuf var_chk;   // stacked check id of each variable's edges (ascending edge order)
+    // stream of the single-phase ABI (mbp_c2v_pass & co.): never the legacy
+    // default stream, so they do not serialise against other streams
+    cudaStream_t op_stream = nullptr;
+    ~mbp_ensemble() { if (op_stream) cudaStreamDestroy(op_stream); }
 };
 
 struct mbp_workspace {
@@ -124,7 +128,7 @@ struct mbp_workspace {
     cudaStream_t own_stream = nullptr;
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;   // host-path pipeline
     static constexpr int kMaxSub = 8;
-    cudaEvent_t ev_in[kMaxSub] = {}, ev_out[kMaxSub] = {}, ev_d2h = nullptr;
+    cudaEvent_t ev_in[kMaxSub] = {}, ev_out[kMaxSub] = {}, ev_fin[kMaxSub] = {}, ev_d2h = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
     int last_B = 0;
     bool timed = false, e2e_timed = false;
@@ -137,6 +141,7 @@ struct mbp_workspace {
         for (int i = 0; i < kMaxSub; ++i) {
             if (ev_in[i]) cudaEventDestroy(ev_in[i]);
             if (ev_out[i]) cudaEventDestroy(ev_out[i]);
+            if (ev_fin[i]) cudaEventDestroy(ev_fin[i]);
         }
         if (ev_d2h) cudaEventDestroy(ev_d2h);
         if (own_stream) cudaStreamDestroy(own_stream);
@@ -232,6 +237,11 @@ int mbp_ensemble_create(int32_t n, int32_t m, int32_t u, const int64_t* chk_ptr,
             return fail(MBP_ECUDA, "no CUDA device " + std::to_string(device));
         }
         ens->sm_count = prop.multiProcessorCount;
+        if (cudaStreamCreateWithFlags(&ens->op_stream, cudaStreamNonBlocking) != cudaSuccess) {
+            delete ens;
+            cudaGetLastError();
+            return fail(MBP_ECUDA, "stream creation failed");
+        }
         if ((rc = ens->chk_ptr.alloc(sizeof(int) * (C + 1))) || (rc = ens->chk_var.alloc(sizeof(int) * E)) ||
             (rc = ens->var_ptr.alloc(sizeof(int) * (n + 1))) || (rc = ens->var_edge.alloc(sizeof(int) * E)) ||
             (rc = ens->deg.alloc(C)) || (rc = ens->chk_ell.alloc(sizeof(int) * (size_t)C * D)) ||
@@ -326,7 +336,9 @@ static int ws_alloc(mbp_workspace* ws)
     if (ws->hist_w.bytes != hist_bytes && (rc = ws->hist_w.alloc(hist_bytes))) return rc;
     // frame compaction (decode.cuh): secondary layout of ceil(G/2) groups;
     // off for the diagnostic modes, which read state by original frame index
-    const bool compaction = ws->G >= 2 && !(ws->cfg.flags & (MBP_RECORD_HISTORY | MBP_KEEP_STATE | MBP_NO_COMPACTION));
+    // off when recording histories (written by original frame index); kept
+    // state stays readable through the slot map (moved_slot)
+    const bool compaction = ws->G >= 2 && !(ws->cfg.flags & (MBP_RECORD_HISTORY | MBP_NO_COMPACTION));
     ws->Gb = compaction ? (ws->G + 1) / 2 : 0;
     {
         const size_t Gb = ws->Gb, Fb = Gb * 32;
@@ -396,7 +408,8 @@ int mbp_workspace_create(mbp_ensemble* ens, int32_t max_frames, const mbp_decode
               cudaEventCreateWithFlags(&ws->ev_d2h, cudaEventDisableTiming) == cudaSuccess;
     for (int i = 0; ok && i < mbp_workspace::kMaxSub; ++i)
         ok = cudaEventCreateWithFlags(&ws->ev_in[i], cudaEventDisableTiming) == cudaSuccess &&
-             cudaEventCreateWithFlags(&ws->ev_out[i], cudaEventDisableTiming) == cudaSuccess;
+             cudaEventCreateWithFlags(&ws->ev_out[i], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&ws->ev_fin[i], cudaEventDisableTiming) == cudaSuccess;
     if (!ok || cudaStreamCreateWithFlags(&ws->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreate(&ws->ev0) != cudaSuccess || cudaEventCreate(&ws->ev1) != cudaSuccess ||
         cudaEventCreate(&ws->ev2) != cudaSuccess || cudaEventCreate(&ws->ev3) != cudaSuccess) {
@@ -588,6 +601,8 @@ static int decode_chunk_scatter(mbp_workspace* ws, const uint8_t* noisy, const u
     A.any_bad = ws->any_bad.as<int>(); A.iters = ws->iters.as<int>();
     A.barrier = ws->barrier.as<unsigned>(); A.work = ws->work.as<unsigned>(); A.sweeps_run = ws->sweeps.as<int>();
     A.ts = ws->ts_cap ? ws->ts.as<unsigned long long>() : nullptr; A.ts_cap = ws->ts_cap;
+    if (ws->ts_cap)   // compaction stamps are written only when a compaction happens
+        MBP_CUDA(cudaMemsetAsync(ws->ts.as<unsigned long long>() + ws->ts_cap - 4, 0, 32, s));
     A.Lmax = ws->sc_Lmax.as<float>();
     A.out_conv = conv; A.out_iters = iters; A.out_mism = mism;
     // the scatter kernel works in log2 units (scatter.cuh)
@@ -668,6 +683,8 @@ static int decode_chunk(mbp_workspace* ws, const uint8_t* noisy, const uint8_t* 
     A.ctrl = ws->ctrl.as<int>();
     A.barrier = ws->barrier.as<unsigned>(); A.work = ws->work.as<unsigned>(); A.sweeps_run = ws->sweeps.as<int>();
     A.ts = ws->ts_cap ? ws->ts.as<unsigned long long>() : nullptr; A.ts_cap = ws->ts_cap;
+    if (ws->ts_cap)   // compaction stamps are written only when a compaction happens
+        MBP_CUDA(cudaMemsetAsync(ws->ts.as<unsigned long long>() + ws->ts_cap - 4, 0, 32, s));
     A.B = B; A.out_conv = conv; A.out_iters = iters; A.out_mism = mism;
     A.max_it = cfg.max_iterations; A.clamp = (Real)cfg.llr_clamp; A.damping = (Real)cfg.damping;
     A.sat = ens->sat;
@@ -710,21 +727,87 @@ static int ensure(DevBuf& b, size_t bytes)
     return b.bytes >= bytes ? MBP_OK : b.alloc(bytes);
 }
 
-// Host-buffer path.  The batch is split into sub-batches whose H2D copies
-// (h2d_stream) and D2H copies (d2h_stream) overlap the decode of their
-// neighbours on the workspace stream -- the decode kernel owns every SM, the
-// copies only the copy engines.  The diagnostic modes (kept state, decision
-// history, phase stamps) read the last decode's buffers, so they decode the
-// batch as one piece.
+// Host-buffer path.
+//
+// Streams (batch > workspace capacity): the batch is decoded in chunks of
+// `cap` frames through a two-slot device staging ring.  Chunk c's H2D copy
+// (h2d_stream) overlaps chunk c-1's decode (workspace stream) and chunk
+// c-2's D2H copy (d2h_stream): the decode kernel owns every SM, the copies
+// only the copy engines, so a long stream runs at the decode rate.
+//
+// Single batches (batch <= cap) may be split into sub-batches that overlap
+// the same way (MBP_HOST_SUBBATCHES; by default only above 1024 frames: the
+// decode kernel's efficiency falls below ~1024 frames per launch).  The
+// diagnostic modes (kept state, decision history, phase stamps) read the
+// last decode's buffers, so they decode a batch as one piece.
+static bool diagnostic(const mbp_workspace* ws)
+{
+    return (ws->cfg.flags & (MBP_KEEP_STATE | MBP_RECORD_HISTORY | MBP_PROFILE_PHASES)) != 0;
+}
+
 static int host_subbatches(const mbp_workspace* ws, int64_t batch)
 {
-    if (ws->cfg.flags & (MBP_KEEP_STATE | MBP_RECORD_HISTORY | MBP_PROFILE_PHASES)) return 1;
-    if (batch > ws->cap) return 1;   // the device path already works in cap-sized chunks
-    // the decode kernel's efficiency falls below ~1024 frames per launch
-    // (fixed per-sweep costs), so only large host batches are split
+    if (diagnostic(ws)) return 1;
     if (const char* v = std::getenv("MBP_HOST_SUBBATCHES"))
         return (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)std::atoi(v), mbp_workspace::kMaxSub, batch / 32}));
     return (int)std::max<int64_t>(1, std::min<int64_t>(mbp_workspace::kMaxSub, batch / 1024));
+}
+
+static int decode_host_stream(mbp_workspace* ws, const uint8_t* noisy, const uint8_t* syn, const double* e,
+                              int32_t e_stride, int64_t batch, uint8_t* corrected, uint8_t* converged,
+                              int32_t* iterations, int32_t* mismatches)
+{
+    const mbp_ensemble* ens = ws->ens;
+    cudaStream_t s = ws->own_stream;
+    const size_t nb = (ens->n + 7) / 8, sb = (size_t)ens->u * ((ens->m + 7) / 8);
+    const int64_t cap = ws->cap;
+    const size_t ne = e_stride ? (size_t)cap : 1;
+    int rc;
+    if ((rc = ensure(ws->tmp_in, 2 * cap * (nb + sb))) || (rc = ensure(ws->tmp_out, 2 * cap * nb)) ||
+        (rc = ensure(ws->tmp_conv, 2 * cap)) || (rc = ensure(ws->tmp_iters, 2 * cap * 4)) ||
+        (rc = ensure(ws->tmp_mism, 2 * cap * 4)) || (rc = ensure(ws->tmp_e, 2 * ne * 8)))
+        return rc;
+    MBP_CUDA(cudaEventRecord(ws->ev2, s));
+    MBP_CUDA(cudaStreamWaitEvent(ws->h2d_stream, ws->ev2, 0));
+    MBP_CUDA(cudaStreamWaitEvent(ws->d2h_stream, ws->ev2, 0));
+    const int64_t chunks = (batch + cap - 1) / cap;
+    for (int64_t c = 0; c < chunks; ++c) {
+        const int k = (int)(c & 1);
+        const int64_t a = c * cap, n = std::min<int64_t>(cap, batch - a);
+        uint8_t* in_noisy = ws->tmp_in.as<uint8_t>() + k * cap * (nb + sb);
+        uint8_t* in_syn = in_noisy + cap * nb;
+        double* in_e = ws->tmp_e.as<double>() + k * ne;
+        uint8_t* out_rows = ws->tmp_out.as<uint8_t>() + k * cap * nb;
+        uint8_t* out_conv = ws->tmp_conv.as<uint8_t>() + k * cap;
+        int* out_it = ws->tmp_iters.as<int>() + k * cap;
+        int* out_mis = ws->tmp_mism.as<int>() + k * cap;
+        // input slot k is free once chunk c-2's decode has run
+        if (c >= 2) MBP_CUDA(cudaStreamWaitEvent(ws->h2d_stream, ws->ev_out[k], 0));
+        MBP_CUDA(cudaMemcpyAsync(in_noisy, noisy + a * nb, n * nb, cudaMemcpyHostToDevice, ws->h2d_stream));
+        MBP_CUDA(cudaMemcpyAsync(in_syn, syn + a * sb, n * sb, cudaMemcpyHostToDevice, ws->h2d_stream));
+        MBP_CUDA(cudaMemcpyAsync(in_e, e + (e_stride ? a : 0), (e_stride ? n : 1) * 8, cudaMemcpyHostToDevice,
+                                 ws->h2d_stream));
+        MBP_CUDA(cudaEventRecord(ws->ev_in[k], ws->h2d_stream));
+        MBP_CUDA(cudaStreamWaitEvent(s, ws->ev_in[k], 0));
+        // output slot k is free once chunk c-2's results reached the host
+        if (c >= 2) MBP_CUDA(cudaStreamWaitEvent(s, ws->ev_fin[k], 0));
+        if ((rc = mbp_decode_batch_device(ws, in_noisy, in_syn, in_e, e_stride, n, out_rows, out_conv, out_it,
+                                          out_mis, s)))
+            return rc;
+        MBP_CUDA(cudaEventRecord(ws->ev_out[k], s));
+        MBP_CUDA(cudaStreamWaitEvent(ws->d2h_stream, ws->ev_out[k], 0));
+        MBP_CUDA(cudaMemcpyAsync(corrected + a * nb, out_rows, n * nb, cudaMemcpyDeviceToHost, ws->d2h_stream));
+        MBP_CUDA(cudaMemcpyAsync(converged + a, out_conv, n, cudaMemcpyDeviceToHost, ws->d2h_stream));
+        MBP_CUDA(cudaMemcpyAsync(iterations + a, out_it, n * 4, cudaMemcpyDeviceToHost, ws->d2h_stream));
+        MBP_CUDA(cudaMemcpyAsync(mismatches + a, out_mis, n * 4, cudaMemcpyDeviceToHost, ws->d2h_stream));
+        MBP_CUDA(cudaEventRecord(ws->ev_fin[k], ws->d2h_stream));
+    }
+    MBP_CUDA(cudaEventRecord(ws->ev_d2h, ws->d2h_stream));
+    MBP_CUDA(cudaStreamWaitEvent(s, ws->ev_d2h, 0));
+    MBP_CUDA(cudaEventRecord(ws->ev3, s));
+    MBP_CUDA(cudaStreamSynchronize(s));
+    ws->e2e_timed = true;
+    return MBP_OK;
 }
 
 int mbp_decode_batch(mbp_workspace* ws, const uint8_t* noisy, const uint8_t* syn, const double* e,
@@ -737,6 +820,8 @@ int mbp_decode_batch(mbp_workspace* ws, const uint8_t* noisy, const uint8_t* syn
     if (batch <= 0) return batch == 0 ? MBP_OK : fail(MBP_EINVAL, "negative batch");
     const mbp_ensemble* ens = ws->ens;
     DeviceGuard dg(ens->device);
+    if (batch > ws->cap && !diagnostic(ws))
+        return decode_host_stream(ws, noisy, syn, e, e_stride, batch, corrected, converged, iterations, mismatches);
     cudaStream_t s = ws->own_stream;
     const size_t nb = (ens->n + 7) / 8, sb = (size_t)ens->u * ((ens->m + 7) / 8);
     const size_t ne = e_stride ? (size_t)batch : 1;
@@ -839,19 +924,35 @@ int mbp_syndrome_batch(mbp_workspace* ws, const uint8_t* keys, int64_t batch, ui
 // ---------------------------------------------------------------------------
 // state readback
 // ---------------------------------------------------------------------------
+// Where the last chunk left `frame`'s state: its slot in the compacted
+// layout (frames still undecided when the chunk compacted, decode.cuh /
+// scatter.cuh sc_compact) or -1 (primary layout, lane = frame).
+static int moved_slot(mbp_workspace* ws, int64_t frame, int* slot)
+{
+    *slot = -1;
+    if (!ws->Gb) return MBP_OK;
+    int v[2] = {0, 0};
+    MBP_CUDA(cudaMemcpy(v, ws->sweeps.p, 8, cudaMemcpyDeviceToHost));
+    if (v[1] == 0) return MBP_OK;   // no compaction in the last chunk
+    MBP_CUDA(cudaMemcpy(slot, ws->newslot.as<int>() + frame, 4, cudaMemcpyDeviceToHost));
+    return MBP_OK;
+}
+
 static int read_lane(mbp_workspace* ws, const void* base, long long count, int64_t frame, double* out,
                      const int* map = nullptr)
 {
     DevBuf tmp;
     int rc;
     if ((rc = tmp.alloc(count * 8))) return rc;
-    const int lane = (int)(frame & 31);
+    const int lane = (int)(frame & 31);   // frame's lane (or compacted slot's)
+    cudaStream_t s = ws->own_stream;
     if (ws->real_size == 8)
-        mbp::gather_lane_kernel<double><<<(int)((count + 255) / 256), 256>>>((const double*)base, count, lane, map, tmp.as<double>());
+        mbp::gather_lane_kernel<double><<<(int)((count + 255) / 256), 256, 0, s>>>((const double*)base, count, lane, map, tmp.as<double>());
     else
-        mbp::gather_lane_kernel<float><<<(int)((count + 255) / 256), 256>>>((const float*)base, count, lane, map, tmp.as<double>());
+        mbp::gather_lane_kernel<float><<<(int)((count + 255) / 256), 256, 0, s>>>((const float*)base, count, lane, map, tmp.as<double>());
     MBP_CUDA(cudaGetLastError());
-    MBP_CUDA(cudaMemcpy(out, tmp.p, count * 8, cudaMemcpyDeviceToHost));
+    MBP_CUDA(cudaMemcpyAsync(out, tmp.p, count * 8, cudaMemcpyDeviceToHost, s));
+    MBP_CUDA(cudaStreamSynchronize(s));
     return MBP_OK;
 }
 
@@ -864,26 +965,31 @@ int mbp_workspace_read_posterior(mbp_workspace* ws, int64_t frame, double* poste
     DeviceGuard dg(ens->device);
     MBP_CUDA(cudaStreamSynchronize(ws->own_stream));
     MBP_CUDA(cudaDeviceSynchronize());
-    const size_t g = frame / 32;
+    int rc, s2;
+    if ((rc = moved_slot(ws, frame, &s2))) return rc;
+    const size_t g = s2 >= 0 ? (size_t)s2 / 32 : frame / 32;
+    const int lane = s2 >= 0 ? (s2 & 31) : (int)(frame & 31);
     if (ws->scatter) {
         // post_t lives in slot t & 1; a frame's last sweep is its converged
         // iteration (0: the prior, kept in slot 0) or max_iterations
         int it = -1;
         MBP_CUDA(cudaMemcpy(&it, ws->iters.as<int>() + frame, 4, cudaMemcpyDeviceToHost));
         const int last = it >= 0 ? it : ws->cfg.max_iterations;
-        const float* base = ws->sc_vb.as<float>() + g * ens->n * mbp::kVB + (size_t)(last & 1) * 32;
+        const float* vb = s2 >= 0 ? ws->sc_vb_b.as<float>() : ws->sc_vb.as<float>();
+        const unsigned* nw = s2 >= 0 ? ws->noisy_b.as<unsigned>() : ws->noisy_w.as<unsigned>();
+        const float* base = vb + g * ens->n * mbp::kVB + (size_t)(last & 1) * 32;
         DevBuf tmp;
-        int rc;
         if ((rc = tmp.alloc((size_t)ens->n * 8))) return rc;
-        gather_rel_post_kernel<<<(ens->n + 255) / 256, 256>>>(base, ws->noisy_w.as<unsigned>() + g * ens->n, ens->n,
-                                                              (int)(frame & 31), tmp.as<double>());
+        gather_rel_post_kernel<<<(ens->n + 255) / 256, 256, 0, ws->own_stream>>>(
+            base, nw + g * ens->n, ens->n, lane, tmp.as<double>());
         MBP_CUDA(cudaGetLastError());
-        MBP_CUDA(cudaMemcpy(posterior, tmp.p, (size_t)ens->n * 8, cudaMemcpyDeviceToHost));
+        MBP_CUDA(cudaMemcpyAsync(posterior, tmp.p, (size_t)ens->n * 8, cudaMemcpyDeviceToHost, ws->own_stream));
+        MBP_CUDA(cudaStreamSynchronize(ws->own_stream));
         return MBP_OK;
     }
     const size_t P = ws->cfg.combining_mode == MBP_ISOLATED_PER_MATRIX ? (size_t)ens->u + 1 : 1;
-    const char* base = ws->post.as<char>() + ((g * P + (P - 1)) * ens->n * 32) * ws->real_size;
-    return read_lane(ws, base, ens->n, frame, posterior);
+    const char* base = (s2 >= 0 ? ws->post_b : ws->post).as<char>() + ((g * P + (P - 1)) * ens->n * 32) * ws->real_size;
+    return read_lane(ws, base, ens->n, lane, posterior);
 }
 
 int mbp_workspace_read_c2v(mbp_workspace* ws, int64_t frame, double* c2v)
@@ -896,20 +1002,27 @@ int mbp_workspace_read_c2v(mbp_workspace* ws, int64_t frame, double* c2v)
     const mbp_ensemble* ens = ws->ens;
     DeviceGuard dg(ens->device);
     MBP_CUDA(cudaDeviceSynchronize());
-    const char* base = ws->c2v.as<char>() + ((size_t)(frame / 32) * ens->C * ens->Ds * 32) * ws->real_size;
-    return read_lane(ws, base, ens->E, frame, c2v, ens->ref2slot.as<int>());
+    int rc, s2;
+    if ((rc = moved_slot(ws, frame, &s2))) return rc;
+    const size_t g = s2 >= 0 ? (size_t)s2 / 32 : frame / 32;
+    const char* base = (s2 >= 0 ? ws->c2v_b : ws->c2v).as<char>() + (g * ens->C * ens->Ds * 32) * ws->real_size;
+    return read_lane(ws, base, ens->E, s2 >= 0 ? s2 : frame, c2v, ens->ref2slot.as<int>());
 }
 
 int mbp_workspace_read_v2c(mbp_workspace* ws, int64_t frame, double* v2c)
 {
     if (!ws || !v2c) return fail(MBP_EINVAL, "null pointer argument");
+    if (!(ws->cfg.flags & MBP_KEEP_STATE)) return fail(MBP_EINVAL, "workspace was not configured with MBP_KEEP_STATE");
     if (!ws->v2c.p) return fail(MBP_EINVAL, "workspace keeps no v2c buffer (damping == 0)");
     if (frame < 0 || frame >= ws->last_B) return fail(MBP_EINVAL, "frame outside the last batch");
     const mbp_ensemble* ens = ws->ens;
     DeviceGuard dg(ens->device);
     MBP_CUDA(cudaDeviceSynchronize());
-    const char* base = ws->v2c.as<char>() + ((size_t)(frame / 32) * ens->C * ens->Ds * 32) * ws->real_size;
-    return read_lane(ws, base, ens->E, frame, v2c, ens->ref2slot.as<int>());
+    int rc, s2;
+    if ((rc = moved_slot(ws, frame, &s2))) return rc;
+    const size_t g = s2 >= 0 ? (size_t)s2 / 32 : frame / 32;
+    const char* base = (s2 >= 0 ? ws->v2c_b : ws->v2c).as<char>() + (g * ens->C * ens->Ds * 32) * ws->real_size;
+    return read_lane(ws, base, ens->E, s2 >= 0 ? s2 : frame, v2c, ens->ref2slot.as<int>());
 }
 
 int mbp_workspace_read_history(mbp_workspace* ws, int64_t frame, int32_t rows, uint8_t* out)
@@ -993,11 +1106,11 @@ static int phase_c2v(mbp_ensemble* ens, int l, const uint8_t* syn_bits, double c
     DevBuf dv, dc, ds;
     int rc;
     if ((rc = dv.alloc(E * sizeof(Real))) || (rc = dc.alloc(E * sizeof(Real))) || (rc = ds.alloc(ens->m))) return rc;
-    MBP_CUDA(cudaMemcpy(dv.p, hv.data(), E * sizeof(Real), cudaMemcpyHostToDevice));
-    MBP_CUDA(cudaMemcpy(dc.p, hc.data(), E * sizeof(Real), cudaMemcpyHostToDevice));
-    MBP_CUDA(cudaMemcpy(ds.p, syn_bits, ens->m, cudaMemcpyHostToDevice));
+    MBP_CUDA(cudaMemcpyAsync(dv.p, hv.data(), E * sizeof(Real), cudaMemcpyHostToDevice, ens->op_stream));
+    MBP_CUDA(cudaMemcpyAsync(dc.p, hc.data(), E * sizeof(Real), cudaMemcpyHostToDevice, ens->op_stream));
+    MBP_CUDA(cudaMemcpyAsync(ds.p, syn_bits, ens->m, cudaMemcpyHostToDevice, ens->op_stream));
     const int lo = l * ens->m, hi = lo + ens->m, grid = (ens->m + 127) / 128;
-#define MBP_C2V(D) mbp::c2v_phase_kernel<Real, D><<<grid, 128>>>(ens->chk_ptr.as<int>(), lo, hi, ds.as<uint8_t>(), (Real)clamp, ens->sat, dv.as<Real>(), dc.as<Real>())
+#define MBP_C2V(D) mbp::c2v_phase_kernel<Real, D><<<grid, 128, 0, ens->op_stream>>>(ens->chk_ptr.as<int>(), lo, hi, ds.as<uint8_t>(), (Real)clamp, ens->sat, dv.as<Real>(), dc.as<Real>())
     switch (pick_degree(ens->dmax_c)) {
     case 8: MBP_C2V(8); break;
     case 16: MBP_C2V(16); break;
@@ -1007,7 +1120,8 @@ static int phase_c2v(mbp_ensemble* ens, int l, const uint8_t* syn_bits, double c
     }
 #undef MBP_C2V
     MBP_CUDA(cudaGetLastError());
-    MBP_CUDA(cudaMemcpy(hc.data(), dc.p, E * sizeof(Real), cudaMemcpyDeviceToHost));
+    MBP_CUDA(cudaMemcpyAsync(hc.data(), dc.p, E * sizeof(Real), cudaMemcpyDeviceToHost, ens->op_stream));
+    MBP_CUDA(cudaStreamSynchronize(ens->op_stream));
     for (size_t k = 0; k < E; ++k) c2v[k] = (double)hc[k];
     return MBP_OK;
 }
@@ -1033,14 +1147,15 @@ static int phase_v2c(mbp_ensemble* ens, int l, int joint, double damping, double
     DevBuf dc, dv, dp;
     int rc;
     if ((rc = dc.alloc(E * sizeof(Real))) || (rc = dv.alloc(E * sizeof(Real))) || (rc = dp.alloc(n * sizeof(Real)))) return rc;
-    MBP_CUDA(cudaMemcpy(dc.p, hc.data(), E * sizeof(Real), cudaMemcpyHostToDevice));
-    MBP_CUDA(cudaMemcpy(dv.p, hv.data(), E * sizeof(Real), cudaMemcpyHostToDevice));
-    MBP_CUDA(cudaMemcpy(dp.p, hp.data(), n * sizeof(Real), cudaMemcpyHostToDevice));
-    mbp::v2c_phase_kernel<Real><<<(int)((n + 127) / 128), 128>>>(
+    MBP_CUDA(cudaMemcpyAsync(dc.p, hc.data(), E * sizeof(Real), cudaMemcpyHostToDevice, ens->op_stream));
+    MBP_CUDA(cudaMemcpyAsync(dv.p, hv.data(), E * sizeof(Real), cudaMemcpyHostToDevice, ens->op_stream));
+    MBP_CUDA(cudaMemcpyAsync(dp.p, hp.data(), n * sizeof(Real), cudaMemcpyHostToDevice, ens->op_stream));
+    mbp::v2c_phase_kernel<Real><<<(int)((n + 127) / 128), 128, 0, ens->op_stream>>>(
         ens->var_ptr.as<int>(), ens->var_edge.as<int>(), (int)n, (int)ens->edge_off[l], (int)ens->edge_off[l + 1],
         joint, (Real)damping, (Real)clamp, dc.as<Real>(), dp.as<Real>(), dv.as<Real>());
     MBP_CUDA(cudaGetLastError());
-    MBP_CUDA(cudaMemcpy(hv.data(), dv.p, E * sizeof(Real), cudaMemcpyDeviceToHost));
+    MBP_CUDA(cudaMemcpyAsync(hv.data(), dv.p, E * sizeof(Real), cudaMemcpyDeviceToHost, ens->op_stream));
+    MBP_CUDA(cudaStreamSynchronize(ens->op_stream));
     for (size_t k = 0; k < E; ++k) v2c[k] = (double)hv[k];
     return MBP_OK;
 }
@@ -1065,12 +1180,13 @@ static int phase_post(mbp_ensemble* ens, const double* c2v, const double* priors
     DevBuf dc, dp, dout;
     int rc;
     if ((rc = dc.alloc(E * sizeof(Real))) || (rc = dp.alloc(n * sizeof(Real))) || (rc = dout.alloc(n * sizeof(Real)))) return rc;
-    MBP_CUDA(cudaMemcpy(dc.p, hc.data(), E * sizeof(Real), cudaMemcpyHostToDevice));
-    MBP_CUDA(cudaMemcpy(dp.p, hp.data(), n * sizeof(Real), cudaMemcpyHostToDevice));
-    mbp::posterior_phase_kernel<Real><<<(int)((n + 127) / 128), 128>>>(ens->var_ptr.as<int>(), ens->var_edge.as<int>(),
+    MBP_CUDA(cudaMemcpyAsync(dc.p, hc.data(), E * sizeof(Real), cudaMemcpyHostToDevice, ens->op_stream));
+    MBP_CUDA(cudaMemcpyAsync(dp.p, hp.data(), n * sizeof(Real), cudaMemcpyHostToDevice, ens->op_stream));
+    mbp::posterior_phase_kernel<Real><<<(int)((n + 127) / 128), 128, 0, ens->op_stream>>>(ens->var_ptr.as<int>(), ens->var_edge.as<int>(),
                                                                        (int)n, dc.as<Real>(), dp.as<Real>(), dout.as<Real>());
     MBP_CUDA(cudaGetLastError());
-    MBP_CUDA(cudaMemcpy(ho.data(), dout.p, n * sizeof(Real), cudaMemcpyDeviceToHost));
+    MBP_CUDA(cudaMemcpyAsync(ho.data(), dout.p, n * sizeof(Real), cudaMemcpyDeviceToHost, ens->op_stream));
+    MBP_CUDA(cudaStreamSynchronize(ens->op_stream));
     for (size_t k = 0; k < n; ++k) post[k] = (double)ho[k];
     return MBP_OK;
 }

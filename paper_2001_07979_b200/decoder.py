@@ -21,6 +21,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 import threading
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -153,20 +154,33 @@ class DeviceEnsemble:
             self.handle = None
 
 
-_DEV_CACHE: dict = {}
+_DEV_CACHE_SIZE = 8
+_DEV_CACHE: "OrderedDict" = OrderedDict()
 _DEV_LOCK = threading.Lock()
 
 
+def _content_key(ensemble) -> tuple:
+    """Identity of a matrix set by content (memoised SHA-256 per matrix):
+    equal graphs share one device upload whatever Python object holds them."""
+    return tuple(h.content_hash() for h in _matrices(ensemble))
+
+
 def device_ensemble(ensemble, device: int = 0) -> DeviceEnsemble:
-    """Upload once per (ensemble object, device); the ensemble is immutable."""
+    """Upload once per (matrix contents, device); the ensemble is immutable.
+    The cache is a bounded LRU -- evicting only drops the cache's reference,
+    a DeviceEnsemble lives as long as the BatchDecoders that use it."""
     if isinstance(ensemble, DeviceEnsemble):
         return ensemble
-    key = (id(ensemble), int(device))
+    key = (_content_key(ensemble), int(device))
     with _DEV_LOCK:
         de = _DEV_CACHE.get(key)
-        if de is None or de._ensemble is not ensemble:
+        if de is None:
             de = DeviceEnsemble(ensemble, device)
             _DEV_CACHE[key] = de
+            while len(_DEV_CACHE) > _DEV_CACHE_SIZE:
+                _DEV_CACHE.popitem(last=False)
+        else:
+            _DEV_CACHE.move_to_end(key)
         return de
 
 
@@ -230,17 +244,48 @@ class BatchDecoder:
         out.converged = out.converged.astype(bool)
         return out
 
-    def decode_device(self, noisy, syn, e, out=None, stream=None):
-        """CUDA-tensor path (inputs resident in HBM); returns device tensors."""
+    def _check_device_tensor(self, t, name, dtype, shape=None):
         import torch
 
+        if not torch.is_tensor(t) or not t.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor")
+        if t.device.index != self.dev.device:
+            raise ValueError(f"{name} is on cuda:{t.device.index}, the ensemble on cuda:{self.dev.device}")
+        if t.dtype != dtype:
+            raise ValueError(f"{name} must have dtype {dtype}, got {t.dtype}")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+        if shape is not None and tuple(t.shape) != tuple(shape):
+            raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+
+    def decode_device(self, noisy, syn, e, out=None, stream=None):
+        """CUDA-tensor path (inputs resident in HBM); returns device tensors.
+
+        ``noisy``/``syn``: contiguous uint8 rows on the ensemble's device; ``e``
+        a float in (0, 0.5) or a contiguous float64 CUDA tensor of 1 or B
+        values (not range-checked: that would need a device sync)."""
+        import torch
+
+        self._check_device_tensor(noisy, "noisy", torch.uint8)
         B = self._check_rows(noisy, syn)
+        self._check_device_tensor(syn, "syn", torch.uint8)
         if not torch.is_tensor(e):
-            e = torch.tensor([float(e)], dtype=torch.float64, device=noisy.device)
+            e = float(e)
+            if not 0.0 < e < 0.5:
+                raise ValueError(f"crossover probability must be in (0, 0.5), got {e}")
+            e = torch.tensor([e], dtype=torch.float64, device=noisy.device)
+        self._check_device_tensor(e, "e", torch.float64)
+        if e.numel() not in (1, B):
+            raise ValueError("e must be a scalar or one value per frame")
         if out is None:
             out = (torch.empty_like(noisy), torch.empty(B, dtype=torch.uint8, device=noisy.device),
                    torch.empty(B, dtype=torch.int32, device=noisy.device),
                    torch.empty(B, dtype=torch.int32, device=noisy.device))
+        else:
+            for t, nm, dt, shp in zip(out, ("corrected", "converged", "iterations", "mismatches"),
+                                      (torch.uint8, torch.uint8, torch.int32, torch.int32),
+                                      (tuple(noisy.shape), (B,), (B,), (B,))):
+                self._check_device_tensor(t, f"out.{nm}", dt, shp)
         s = stream if stream is not None else torch.cuda.current_stream(noisy.device).cuda_stream
         N.call("mbp_decode_batch_device", self.handle, noisy.data_ptr(), syn.data_ptr(), e.data_ptr(),
                0 if e.numel() == 1 else 1, B, out[0].data_ptr(), out[1].data_ptr(), out[2].data_ptr(),
@@ -252,9 +297,13 @@ class BatchDecoder:
         if hasattr(keys, "is_cuda") and keys.is_cuda:
             import torch
 
+            self._check_device_tensor(keys, "keys", torch.uint8)
             B = keys.shape[0]
+            if keys.shape != (B, self.dev.nbytes_key):
+                raise ValueError(f"key rows must be [B, {self.dev.nbytes_key}] bytes")
             if out is None:
                 out = torch.empty((B, self.dev.nbytes_syn), dtype=torch.uint8, device=keys.device)
+            self._check_device_tensor(out, "out", torch.uint8, (B, self.dev.nbytes_syn))
             s = stream if stream is not None else torch.cuda.current_stream(keys.device).cuda_stream
             N.call("mbp_syndrome_batch_device", self.handle, keys.data_ptr(), B, out.data_ptr(), C.c_void_p(s))
             return out
@@ -409,24 +458,34 @@ def _matrices(ensemble_or_matrix):
 
 
 def compute_syndrome(matrix, key) -> BitBlock:
-    """z_j = XOR of key bits over check j (Eq. 1) -- on the GPU."""
+    """z_j = XOR of key bits over check j (Eq. 1) -- on the GPU.  Thread-safe:
+    the reference calls it from worker threads (bench._frame_inputs), so each
+    cached syndrome workspace is used under its own lock."""
     if key.length != matrix.n:
         raise ValueError(f"key length {key.length} != n={matrix.n}")
-    dec = _syndrome_decoder(matrix)
-    rows = dec.syndromes(np.asarray(key.data, dtype=np.uint8).reshape(1, -1))
+    dec, lock = _syndrome_decoder(matrix)
+    with lock:
+        rows = dec.syndromes(np.asarray(key.data, dtype=np.uint8).reshape(1, -1))
     return BitBlock(rows[0, : (matrix.m + 7) // 8].copy(), matrix.m)
 
 
-_SYN_CACHE: dict = {}
+_SYN_CACHE: "OrderedDict" = OrderedDict()
+_SYN_LOCK = threading.Lock()
 
 
-def _syndrome_decoder(matrix) -> BatchDecoder:
-    key = id(matrix)
-    dec = _SYN_CACHE.get(key)
-    if dec is None or dec.dev._ensemble is not matrix:
-        dec = BatchDecoder(matrix, 32)
-        _SYN_CACHE[key] = dec
-    return dec
+def _syndrome_decoder(matrix):
+    """(BatchDecoder, lock) per matrix contents; bounded LRU like _DEV_CACHE."""
+    key = _content_key(matrix)
+    with _SYN_LOCK:
+        ent = _SYN_CACHE.get(key)
+        if ent is None:
+            ent = (BatchDecoder(matrix, 32), threading.Lock())
+            _SYN_CACHE[key] = ent
+            while len(_SYN_CACHE) > _DEV_CACHE_SIZE:
+                _SYN_CACHE.popitem(last=False)
+        else:
+            _SYN_CACHE.move_to_end(key)
+        return ent
 
 
 def init_priors(noisy_key, e: float) -> np.ndarray:

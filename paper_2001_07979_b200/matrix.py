@@ -47,7 +47,7 @@ class ParityCheckMatrix:
     sorted, no parallel edges, no empty column.  Arrays are read-only.
     """
 
-    __slots__ = ("n", "m", "chk_ptr", "chk_var", "var_ptr", "var_chk")
+    __slots__ = ("n", "m", "chk_ptr", "chk_var", "var_ptr", "var_chk", "_hash")
 
     def __init__(self, n, m, chk_ptr, chk_var, var_ptr, var_chk):
         self.n = int(n)
@@ -58,6 +58,7 @@ class ParityCheckMatrix:
         self.var_chk = np.asarray(var_chk, dtype=np.int32)
         for a in (self.chk_ptr, self.chk_var, self.var_ptr, self.var_chk):
             a.setflags(write=False)
+        self._hash = None
 
     @classmethod
     def from_check_adjacency(cls, n: int, m: int, rows) -> "ParityCheckMatrix":
@@ -110,12 +111,15 @@ class ParityCheckMatrix:
 
     def content_hash(self) -> str:
         """SHA-256 over (n, m, chk_ptr, chk_var); equals the reference's
-        ``ParityCheckMatrix.content_hash`` (matrix.py:148-154) for the same graph."""
-        h = hashlib.sha256()
-        h.update(np.array([self.n, self.m], dtype="<i8").tobytes())
-        h.update(self.chk_ptr.astype("<i8").tobytes())
-        h.update(self.chk_var.astype("<i4").tobytes())
-        return h.hexdigest()
+        ``ParityCheckMatrix.content_hash`` (matrix.py:148-154) for the same graph.
+        Memoised: the arrays are read-only."""
+        if self._hash is None:
+            h = hashlib.sha256()
+            h.update(np.array([self.n, self.m], dtype="<i8").tobytes())
+            h.update(self.chk_ptr.astype("<i8").tobytes())
+            h.update(self.chk_var.astype("<i4").tobytes())
+            self._hash = h.hexdigest()
+        return self._hash
 
     def __eq__(self, other):
         if not hasattr(other, "chk_var"):
