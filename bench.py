@@ -1,16 +1,34 @@
 """Reconciliation throughput of the B200 MBP decoder (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU)
 
-Workload (BASELINE.json configs[1]): u=2 PEG matrices
-n=65536, m=32768 (R=0.5, the reference's build_ensemble(..., base_seed=1)),
-BSC QBER e=0.03, a 1024-frame batch per GPU; frames are the reference's own
-counter-based streams (_frame_inputs, bench.py:123-130) for frame indices
-rank*1024 + i.  A step = one batched decode of the rank's 1024 frames with
-noisy keys and syndromes already resident in HBM.  Metric = corrected Mbps:
-n * #(converged and corrected == key) / time (bench.py:188-195), summed over
-ranks, divided by the max over ranks of the device-timed step total.
+``--gpus N`` with N > 1 launches N ranks itself (torch.distributed.run on
+127.0.0.1); under an external torchrun the ranks come from the environment.
+One process per GPU; when there are fewer GPUs than ranks, ranks share GPUs
+round-robin and the reductions run over gloo (said in ``config``).
+
+Headline (BASELINE.json configs[1]): u=2 PEG matrices
+n=65536, m=32768 (R=1/2, the reference's build_ensemble(..., base_seed=1)),
+BSC QBER e=0.03, a 1024-frame batch per GPU.  Frames are the reference's own
+counter-based streams (_frame_inputs, bench.py:123-130), generated on the
+device bit for bit (csrc/frames.cuh; spot-checked against numpy here).  A
+step = one batched decode of the rank's 1024 frames with noisy keys and
+syndromes resident in HBM.  Metric = corrected Mbps: n * #(converged and
+corrected == key) / time (bench.py:188-195), summed over ranks, divided by
+the max over ranks of the device-timed total.
+
+Also in the line:
+* ``e2e``: the same K steps through the C ABI's host call mbp_decode_batch
+  with pinned host buffers -- every step's H2D copy and result D2H inside the
+  timed region, pipelined against the neighbouring steps' decodes (one call
+  over the K batches); ``e2e.per_call``: K separate 1024-frame calls;
+* ``stream``: BASELINE configs[4], a fixed 65,536-frame stream sharded
+  contiguously over the ranks (strong scaling), device-resident and e2e;
+* ``configs``: the north-star operating point cfg 3 (u=3, m=14650, f=1.15 at
+  e=0.03) and the fp64 parity mode on cfg 2;
+* ``roofline`` of the decode kernel, ``cpu_baseline`` (the reference
+  algorithm on the host cores) and ``parity`` (every frame the CPU leg
+  decodes compared with the GPU's outputs).
 
 ``--impl reference`` times the reference algorithm on the host cores instead
 (oracle/ -- the C restatement of the reference's numba decode, pinned to its
@@ -23,6 +41,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -36,6 +55,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 N_DEFAULT_FRAMES = 1024
+STREAM_FRAMES = 65536          # BASELINE configs[4]
 WORKLOAD = "cfg2"
 E_DEFAULT = 0.03
 # BASELINE.json configs: the headline is cfg2 (configs[1]); the others are
@@ -48,6 +68,7 @@ WORKLOADS = {
     "cfg4": (None, "u=2 n=1048576 m=524288 R=0.5 SYNTHETIC random (3,6)-regular graphs (seeds 7,8)"),
 }
 L2_FLUSH_BYTES = 256 << 20   # > 126 MB L2: written between timed steps
+KERNELS_PER_DECODE = 5       # setup, 2 row->word transposes, decode, word->row transpose
 
 
 def parse():
@@ -57,10 +78,13 @@ def parse():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
     p.add_argument("--frames", type=int, default=N_DEFAULT_FRAMES, help="frames per GPU per step")
+    p.add_argument("--stream", type=int, default=STREAM_FRAMES,
+                   help="frames of the strong-scaling stream (configs[4]); 0 skips it")
     p.add_argument("--e", type=float, default=E_DEFAULT)
     p.add_argument("--precision", choices=("fp32", "fp64"), default="fp32")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-sweep", action="store_true", help="skip the QBER 2-5%% side sweep")
+    p.add_argument("--no-extra", action="store_true", help="skip the cfg3 / fp64 side configurations")
     p.add_argument("--workload", choices=tuple(WORKLOADS), default=WORKLOAD,
                    help="BASELINE config to time (default cfg2 = configs[1], the headline)")
     return p.parse_args()
@@ -69,6 +93,45 @@ def parse():
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def self_launch(nproc: int) -> int:
+    """`python bench.py --gpus N` without torchrun: start N ranks on this node."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
+
+
+def physical_cores() -> int:
+    """Physical cores (unique (package, core) pairs of /proc/cpuinfo)."""
+    try:
+        pairs, phys, core = set(), None, None
+        for line in open("/proc/cpuinfo"):
+            k, _, v = line.partition(":")
+            k = k.strip()
+            if k == "physical id":
+                phys = v.strip()
+            elif k == "core id":
+                core = v.strip()
+            elif not k and phys is not None:
+                pairs.add((phys, core))
+                phys = core = None
+        if phys is not None:
+            pairs.add((phys, core))
+        return len(pairs) or (os.cpu_count() or 1)
+    except OSError:
+        return os.cpu_count() or 1
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
 
 
 def alg_bytes_per_frame(n, m, u, E, iters):
@@ -179,31 +242,95 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples), "source": self.source}
 
 
-def load_workload(rank, frames, e, world=1, workload=WORKLOAD):
-    """Rank's shard of the frame stream: frames [rank*B, (rank+1)*B) of the
-    reference's counter-based streams (shard.shard_range over world*B frames,
-    weak scaling: B frames per GPU)."""
-    from paper_2001_07979_b200.channel import make_frames
+def load_ensemble_for(workload):
     from paper_2001_07979_b200.matrix import load_ensemble, random_regular_ensemble
-    from paper_2001_07979_b200.shard import shard_range
 
     fname = WORKLOADS[workload][0]
-    ens = (load_ensemble(ROOT / "paper_2001_07979_b200" / "ensembles" / fname) if fname
-           else random_regular_ensemble(1 << 20, 1 << 19, 2, seed=7))
-    lo, hi = shard_range(world * frames, world, rank)
-    fb = make_frames(ens.n, e, hi - lo, seed=0, start=lo)
-    return ens, fb
+    return (load_ensemble(ROOT / "paper_2001_07979_b200" / "ensembles" / fname) if fname
+            else random_regular_ensemble(1 << 20, 1 << 19, 2, seed=7))
+
+
+def device_frames(dec, n, e, lo, count, device):
+    """Frames lo .. lo+count-1 of the point (path ()) in HBM: keys, noisy,
+    syndromes (all on the current stream)."""
+    from paper_2001_07979_b200.channel import make_frames_device
+
+    keys, noisy = make_frames_device(n, e, count, seed=0, start=lo, device=device)
+    return keys, noisy, dec.syndromes(keys)
+
+
+def spot_check_frames(keys, noisy, n, e, lo):
+    """The device generator against numpy's streams on two frames."""
+    from paper_2001_07979_b200.channel import make_frames
+
+    B = keys.shape[0]
+    for k in sorted({0, B - 1}):
+        ref = make_frames(n, e, 1, seed=0, start=lo + k)
+        if not (np.array_equal(keys[k].cpu().numpy(), ref.keys[0])
+                and np.array_equal(noisy[k].cpu().numpy(), ref.noisy[0])):
+            raise RuntimeError(f"device frame generator differs from numpy on frame {lo + k}")
+
+
+def good_bits(out, keys, n):
+    """n * #(converged and corrected == key) (bench.py:188-195), on device."""
+    import torch
+
+    ok = (out[1] != 0) & torch.all(out[0] == keys, dim=1)
+    return int(ok.sum().item()) * n
+
+
+class Pinned:
+    """Pinned host rows (torch pinned memory viewed as numpy)."""
+
+    def __init__(self, shape, dtype):
+        import torch
+
+        tdt = {np.uint8: torch.uint8, np.int32: torch.int32}[np.dtype(dtype).type]
+        self.t = torch.empty(shape, dtype=tdt, pin_memory=True)
+        self.a = self.t.numpy()
+
+
+def time_device_steps(dec, noisy, syn, e_d, out, steps, flush, stream):
+    """K decode steps bracketed by CUDA events on the launching stream, L2
+    flushed before each; returns (per-step ms, per-step decode-kernel ms)."""
+    import torch
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    kernel_ms = []
+    for k in range(steps):
+        flush.fill_(k & 0xFF)
+        starts[k].record(stream)
+        dec.decode_device(noisy, syn, e_d, out=out)
+        ends[k].record(stream)
+        kernel_ms.append(dec.last_timing()[0])
+    torch.cuda.synchronize()
+    return [s.elapsed_time(t) for s, t in zip(starts, ends)], kernel_ms
+
+
+def host_call(dec, noisy_h, syn_h, e, out):
+    """One host-buffer call through the C ABI: (device-event ms, host wall ms)."""
+    t0 = time.perf_counter()
+    dec.decode(noisy_h, syn_h, e, out=out)
+    wall = (time.perf_counter() - t0) * 1e3
+    return dec.last_timing(e2e=True)[1], wall
+
+
+def host_result(B, nb, n):
+    from paper_2001_07979_b200.decoder import BatchResult
+
+    return BatchResult(Pinned((B, nb), np.uint8).a, Pinned((B,), np.uint8).a, Pinned((B,), np.int32).a,
+                       Pinned((B,), np.int32).a, n)
 
 
 def cpu_decode_sample(ens, noisy_rows, syn_rows, e, budget_s=10.0, threads=None):
     """The reference algorithm (oracle/, C restatement of _kernels.decode_loop)
-    on the host cores over a bounded prefix of the frames; returns (Mbps, info)."""
+    on the host cores over a bounded prefix of the frames."""
     import oracle
     from paper_2001_07979_b200.matrix import stacked_layout
 
-    threads = threads or os.cpu_count() or 1
+    threads = threads or host_threads()
     og = oracle.OracleGraph(stacked_layout(ens))
-    # calibrate on one frame per thread, then size the sample to ~budget_s
     B = noisy_rows.shape[0]
     k = min(B, threads)
     t0 = time.perf_counter()
@@ -211,28 +338,52 @@ def cpu_decode_sample(ens, noisy_rows, syn_rows, e, budget_s=10.0, threads=None)
     per_round = max(time.perf_counter() - t0, 1e-3)
     frames = int(min(B, max(k, k * budget_s / per_round)))
     t0 = time.perf_counter()
-    corrected, conv, iters, _ = oracle.decode_batch(og, noisy_rows[:frames], syn_rows[:frames], e, threads=threads)
+    corrected, conv, iters, mism = oracle.decode_batch(og, noisy_rows[:frames], syn_rows[:frames], e,
+                                                       threads=threads)
     wall = time.perf_counter() - t0
-    return corrected, conv, iters, wall, frames, threads
+    return corrected, conv, iters, mism, wall, frames, threads
+
+
+def traffic_record(workload, frames, e):
+    """ncu DRAM bytes per decode launch for this source tree (None if the
+    committed capture was taken on other sources)."""
+    from paper_2001_07979_b200.build import source_hash
+
+    tf = ROOT / "profiles" / "decode_traffic.json"
+    if not tf.exists():
+        return None
+    try:
+        recs = json.loads(tf.read_text())
+        recs = recs if isinstance(recs, list) else [recs]
+        src = source_hash()
+        for t in recs:
+            if (t.get("workload") == workload and t.get("frames") == frames and t.get("e") == e
+                    and t.get("src_sha") == src):
+                return t
+    except Exception:
+        pass
+    return None
 
 
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    ens, fb = load_workload(0, args.frames, args.e, 1, args.workload)
     import oracle
+    from paper_2001_07979_b200.channel import make_frames_native
     from paper_2001_07979_b200.matrix import stacked_layout
 
+    ens = load_ensemble_for(args.workload)
+    fb = make_frames_native(ens.n, args.e, args.frames, seed=0, start=0)
     lay = stacked_layout(ens)
     og = oracle.OracleGraph(lay)
     syn = np.stack([np.concatenate([np.packbits(
         oracle.syndrome(lay.chk_ptr, lay.chk_var, np.unpackbits(fb.keys[k], count=ens.n, bitorder="little"),
                         l * ens.m, (l + 1) * ens.m), bitorder="little") for l in range(ens.u)])
         for k in range(fb.batch)])
-    threads = os.cpu_count() or 1
+    threads = host_threads()
     step_frames = min(fb.batch, threads * 8)
-    times, good_bits = [], []
+    times, gbits = [], []
     for s in range(args.warmup + args.steps):
         lo = (s * step_frames) % fb.batch
         idx = np.arange(lo, lo + step_frames) % fb.batch
@@ -242,62 +393,224 @@ def run_reference(args):
         if s >= args.warmup:
             good = conv & np.all(corrected == fb.keys[idx], axis=1)
             times.append(dt)
-            good_bits.append(int(good.sum()) * ens.n)
+            gbits.append(int(good.sum()) * ens.n)
     total = sum(times)
-    value = sum(good_bits) / total / 1e6
+    value = sum(gbits) / total / 1e6
     line = {
         "metric": "reconciliation throughput (corrected Mbps)", "value": round(value, 4), "unit": "Mbps",
         "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * total / len(times), 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference Philox frame streams)",
-        "config": config_dict(args, ens),
-        "cpu_baseline": {"value": round(value, 4), "unit": "Mbps", "cores": threads, "kind": "port",
+        "config": config_dict(args, ens, args.gpus, args.gpus),
+        "cpu_baseline": {"value": round(value, 4), "unit": "Mbps", "cores": physical_cores(), "threads": threads,
+                         "kind": "port",
                          "sample": f"{step_frames} frames per step of the {args.frames}-frame workload, "
-                                   f"oracle/mbp_oracle.c decode_loop restatement on {threads} POSIX threads"},
+                                   f"oracle/mbp_oracle.c decode_loop restatement (fp64, libm) on {threads} "
+                                   f"POSIX threads"},
         "e2e": {"value": round(value, 4), "unit": "Mbps", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def config_dict(args, ens):
+def config_dict(args, ens, world, devices):
     from paper_2001_07979_b200.channel import efficiency
 
+    par = f"dp{world} (contiguous frame shards, no collective on the data path)"
+    if devices < world:
+        par += f"; {world} ranks on {devices} GPU(s), round-robin"
     return {"workload": f"{args.workload}: {WORKLOADS[args.workload][1]}, "
                         f"BSC e={args.e}, {args.frames}-frame batch per GPU",
             "n": ens.n, "m": ens.m, "u": ens.u, "e": args.e, "f": round(efficiency(ens.m, ens.n, args.e), 4),
             "frames_per_gpu": args.frames, "max_iterations": 60, "llr_clamp": 30.0,
-            "precision": args.precision, "parallelism": f"dp{args.gpus} (frame shards, no collective)",
-            "l2": "flushed between timed steps (256 MiB write); working set >> L2"}
+            "parallelism": par, "l2": "flushed between timed steps (256 MiB write); working set >> L2"}
 
 
-def main():
-    args = parse()
-    if args.impl == "reference":
-        return run_reference(args)
-
+def side_config(workload, e, precision, frames, steps, device, flush, stream):
+    """A single-GPU figure for another configuration: device value, e2e
+    (host call, pipelined over `steps` batches), fer, iterations, kernel ms."""
     import torch
-
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=dev)
 
     from paper_2001_07979_b200 import BatchDecoder, DecoderConfig
 
-    ens, fb = load_workload(rank, args.frames, args.e, world, args.workload)
+    ens = load_ensemble_for(workload)
+    n = ens.n
+    dec = BatchDecoder(ens, frames, DecoderConfig(precision=precision), device=device)
+    keys, noisy, syn = device_frames(dec, n, e, 0, frames, device)
+    e_d = torch.tensor([e], dtype=torch.float64, device=noisy.device)
+    out = dec.decode_device(noisy, syn, e_d)
+    dec.decode_device(noisy, syn, e_d, out=out)
+    torch.cuda.synchronize()
+    step_ms, kms = time_device_steps(dec, noisy, syn, e_d, out, steps, flush, stream)
+    gb = good_bits(out, keys, n)
+    iters = out[2].cpu().numpy()
+    value = gb * steps / (sum(step_ms) / 1e3) / 1e6
+    E = int(ens.matrices[0].edge_count) * ens.u
+    alg = float(sum(alg_bytes_per_frame(n, ens.m, ens.u, E, int(i)) for i in iters))
+    peak, _ = measured_peak_hbm()
+    # e2e: `steps` batches through one host call
+    nb = keys.shape[1]
+    K = steps
+    kk, nn, ss = device_frames(dec, n, e, 0, K * frames, device)
+    noisy_h, syn_h = Pinned(tuple(nn.shape), np.uint8), Pinned(tuple(ss.shape), np.uint8)
+    noisy_h.t.copy_(nn)
+    syn_h.t.copy_(ss)
+    keys_h = kk.cpu().numpy()
+    del kk, nn, ss
+    res = host_result(K * frames, nb, n)
+    host_call(dec, noisy_h.a, syn_h.a, e, res)
+    ev_ms, wall_ms = host_call(dec, noisy_h.a, syn_h.a, e, res)
+    g2 = int((res.converged.astype(bool) & np.all(res.corrected == keys_h, axis=1)).sum()) * n
+    return {
+        "workload": WORKLOADS[workload][1], "e": e, "precision": precision, "frames": frames,
+        "value": round(value, 3), "unit": "Mbps", "ms_per_step": round(statistics.mean(step_ms), 4),
+        "kernel_ms": round(statistics.mean(kms), 4),
+        "e2e": {"value": round(g2 / (ev_ms / 1e3) / 1e6, 3), "host_wall_value": round(g2 / (wall_ms / 1e3) / 1e6, 3),
+                "batches": K},
+        "fer": round(1.0 - float(out[1].float().mean().item()), 6),
+        "mean_iterations": round(float(iters.mean()), 4),
+        "roofline": {"achieved": round(alg / (statistics.mean(kms) / 1e3) / 1e9, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(alg / (statistics.mean(kms) / 1e3) / 1e9 / peak, 4),
+                     "basis": "SURVEY 8(d) message-streaming bytes / decode-kernel time"},
+    }
+
+
+def run_stream(args, ens, dec, rank, world, device, flush, stream):
+    """BASELINE configs[4]: a fixed stream of args.stream frames sharded
+    contiguously over the ranks (strong scaling).  Device-resident value and
+    e2e through the pipelined host call, both max over ranks."""
+    import torch
+
+    from paper_2001_07979_b200.shard import reduce_work_time, shard_range
+
+    n = ens.n
+    lo, hi = shard_range(args.stream, world, rank)
+    S = hi - lo
+    e_d = torch.tensor([args.e], dtype=torch.float64, device=torch.device("cuda", device))
+    keys, noisy, syn = device_frames(dec, n, args.e, lo, max(S, 1), device)
+    out = dec.decode_device(noisy[:S], syn[:S], e_d) if S else None
+    torch.cuda.synchronize()
+    passes = 3
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    flush.fill_(1)
+
+    def run():
+        t0.record(stream)
+        for _ in range(passes):
+            if S:
+                dec.decode_device(noisy[:S], syn[:S], e_d, out=out)
+        t1.record(stream)
+
+    span, _ = job_span(world, run)
+    dev_ms = (span if _SHARED else t0.elapsed_time(t1)) / passes
+    gb = good_bits(out, keys[:S], n) if S else 0
+    # e2e: host pinned buffers through one mbp_decode_batch call per pass
+    nb = keys.shape[1]
+    noisy_h = Pinned((max(S, 1), nb), np.uint8)
+    syn_h = Pinned((max(S, 1), syn.shape[1]), np.uint8)
+    noisy_h.t.copy_(noisy)
+    syn_h.t.copy_(syn)
+    keys_h = keys.cpu().numpy()
+    del keys, noisy, syn
+    res = host_result(max(S, 1), nb, n)
+    ev, wall = [], []
+
+    def run_host():
+        for p in range(passes):
+            if S:
+                a, b = host_call(dec, noisy_h.a[:S], syn_h.a[:S], args.e, res)
+                ev.append(a)
+                wall.append(b)
+
+    span, _ = job_span(world, run_host)
+    if _SHARED:
+        ev, wall = [span / passes], [span / passes]
+    e2e_ms = statistics.mean(ev) if ev else 0.0
+    wall_ms = statistics.mean(wall) if wall else 0.0
+    g2 = int((res.converged[:S].astype(bool) & np.all(res.corrected[:S] == keys_h[:S], axis=1)).sum()) * n
+    (gb_all, g2_all, frames_all), (dev_max, e2e_max, wall_max) = reduce_work_time(
+        [float(gb), float(g2), float(S)], [dev_ms, e2e_ms, wall_ms], device=red_device(device))
+    return {
+        "workload": f"BASELINE configs[4]: {WORKLOADS['cfg2'][1]}, e={args.e}, {args.stream}-frame stream "
+                    f"(frames 0..{args.stream - 1}) in contiguous shards over {world} rank(s)",
+        "frames": int(frames_all), "scaling": "strong",
+        "value": round(gb_all / (dev_max / 1e3) / 1e6, 3), "unit": "Mbps", "ms": round(dev_max, 3),
+        "e2e": {"value": round(g2_all / (e2e_max / 1e3) / 1e6, 3),
+                "host_wall_value": round(g2_all / (wall_max / 1e3) / 1e6, 3),
+                "h2d_bytes": int(args.stream * (nb + dec.dev.nbytes_syn + 8)),
+                "d2h_bytes": int(args.stream * (nb + 9)),
+                "timing": "one mbp_decode_batch host call per rank and pass (pinned buffers, H2D || decode || "
+                          "D2H over 1024-frame chunks); max over ranks"},
+        "fer": round(1.0 - gb_all / max(frames_all * n, 1), 6),
+    }
+
+
+_RED_DEVICE = None
+_SHARED = False     # ranks share GPUs: time the job span, not per-rank events
+
+
+def job_span(world, fn):
+    """(ms, fn()) between two barrier-synchronised host clock reads: the
+    whole job's span when several ranks' kernels time-slice one GPU (their
+    per-rank CUDA-event windows then do not overlap)."""
+    import torch
+
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = fn()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    return (time.perf_counter() - t0) * 1e3, r
+
+
+def red_device(device):
+    return _RED_DEVICE if _RED_DEVICE is not None else device
+
+
+def main():
+    global _RED_DEVICE, _SHARED
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return self_launch(args.gpus)
+
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    ndev = torch.cuda.device_count()
+    if ndev < 1:
+        raise RuntimeError("no CUDA device: the decoder has no CPU fallback")
+    device = local % ndev
+    devices = min(world, ndev)
+    torch.cuda.set_device(device)
+    dev = torch.device("cuda", device)
+    if world > 1:
+        if world <= ndev:
+            dist.init_process_group("nccl", device_id=dev)
+        else:   # ranks share GPUs: NCCL allows one rank per GPU
+            dist.init_process_group("gloo")
+            _RED_DEVICE = torch.device("cpu")
+            _SHARED = True
+
+    from paper_2001_07979_b200 import BatchDecoder, DecoderConfig
+    from paper_2001_07979_b200.shard import reduce_work_time, shard_range
+
+    ens = load_ensemble_for(args.workload)
     n, m, u = ens.n, ens.m, ens.u
-    B = fb.batch
-    dec = BatchDecoder(ens, B, DecoderConfig(precision=args.precision), device=local)
-    keys_d = torch.from_numpy(fb.keys).to(dev)
-    noisy_d = torch.from_numpy(fb.noisy).to(dev)
-    syn_d = dec.syndromes(keys_d)
+    B = args.frames
+    dec = BatchDecoder(ens, B, DecoderConfig(precision=args.precision), device=device)
+    lo, _ = shard_range(world * B, world, rank)
+    keys_d, noisy_d, syn_d = device_frames(dec, n, args.e, lo, B, device)
+    torch.cuda.synchronize()
+    spot_check_frames(keys_d, noisy_d, n, args.e, lo)
     e_d = torch.tensor([args.e], dtype=torch.float64, device=dev)
-    out = (torch.empty_like(noisy_d), torch.empty(B, dtype=torch.uint8, device=dev),
-           torch.empty(B, dtype=torch.int32, device=dev), torch.empty(B, dtype=torch.int32, device=dev))
+    out = dec.decode_device(noisy_d, syn_d, e_d)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -305,156 +618,167 @@ def main():
         dec.decode_device(noisy_d, syn_d, e_d, out=out)
     torch.cuda.synchronize(dev)
 
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    kernel_ms = []
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize(dev)
-    with ClockSampler(local) as clocks:
-        for k in range(args.steps):
-            flush.fill_(k & 0xFF)
-            starts[k].record(stream)
-            dec.decode_device(noisy_d, syn_d, e_d, out=out)
-            ends[k].record(stream)
-            kms, _sw = dec.last_timing()
-            kernel_ms.append(kms)
-        torch.cuda.synchronize(dev)
-    if world > 1:
-        torch.distributed.barrier()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = sum(step_ms)
+    with ClockSampler(device) as clocks:
+        span, (step_ms, kernel_ms) = job_span(world, lambda: time_device_steps(
+            dec, noisy_d, syn_d, e_d, out, args.steps, flush, stream))
+    total_ms = span if _SHARED else sum(step_ms)
     _, sweeps = dec.last_timing()
 
     corrected = out[0].cpu().numpy()
     conv = out[1].cpu().numpy().astype(bool)
     iters = out[2].cpu().numpy()
-    good = conv & np.all(corrected == fb.keys, axis=1)
-    good_bits = int(good.sum()) * n * args.steps
+    mism = out[3].cpu().numpy()
+    keys_h = keys_d.cpu().numpy()
+    good = conv & np.all(corrected == keys_h, axis=1)
+    gbits = int(good.sum()) * n * args.steps
 
-    # ---- e2e: host pinned buffers through the C-ABI host call --------------
-    from paper_2001_07979_b200.decoder import BatchResult
+    # ---- e2e: the K steps' batches (frames of this rank's shard of K*B*world)
+    #      through the host C-ABI call with pinned buffers ---------------------
+    K = args.steps
+    lo_k, _ = shard_range(world * K * B, world, rank)
+    kk, nn, ss = device_frames(dec, n, args.e, lo_k, K * B, device)
+    nb = nn.shape[1]
+    pin_noisy, pin_syn = Pinned((K * B, nb), np.uint8), Pinned((K * B, ss.shape[1]), np.uint8)
+    pin_noisy.t.copy_(nn)
+    pin_syn.t.copy_(ss)
+    keys_k = kk.cpu().numpy()
+    del kk, nn, ss
+    res = host_result(K * B, nb, n)
+    host_call(dec, pin_noisy.a, pin_syn.a, args.e, res)          # warm the staging ring
+    span, (e2e_ms, e2e_wall) = job_span(world, lambda: host_call(dec, pin_noisy.a, pin_syn.a, args.e, res))
+    if _SHARED:
+        e2e_ms = e2e_wall = span
+    e2e_good = int((res.converged.astype(bool) & np.all(res.corrected == keys_k, axis=1)).sum()) * n
+    # per call: K separate 1024-frame host calls (no overlap inside a call)
+    res1 = host_result(B, nb, n)
+    pc_ev, pc_wall, pc_good = [], [], 0
 
-    pin_noisy = torch.from_numpy(fb.noisy).pin_memory().numpy()
-    pin_syn = syn_d.cpu().pin_memory().numpy()
-    # caller-owned pinned result buffers (BatchDecoder.decode's `out`)
-    pin_out = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
-    out_host = BatchResult(pin_out(np.empty_like(fb.noisy)), pin_out(np.empty(B, dtype=np.uint8)),
-                           pin_out(np.empty(B, dtype=np.int32)), pin_out(np.empty(B, dtype=np.int32)), n)
-    conv_buf = out_host.converged
-    e2e_steps = max(3, min(args.steps, 10))
-    e2e_ms = []
-    res = None
-    for k in range(2 + e2e_steps):
-        flush.fill_(k & 0xFF)
-        torch.cuda.synchronize(dev)
-        out_host.converged = conv_buf
-        res = dec.decode(pin_noisy, pin_syn, args.e, out=out_host)
-        if k >= 2:
-            e2e_ms.append(dec.last_timing(e2e=True)[1])
-    e2e_good = int((res.converged & np.all(res.corrected == fb.keys, axis=1)).sum()) * n
-    e2e_total_ms = sum(e2e_ms)
+    def per_call():
+        nonlocal pc_good
+        for k in range(K):
+            a, b = host_call(dec, pin_noisy.a[k * B:(k + 1) * B], pin_syn.a[k * B:(k + 1) * B], args.e, res1)
+            pc_ev.append(a)
+            pc_wall.append(b)
+            pc_good += int((res1.converged.astype(bool)
+                            & np.all(res1.corrected == keys_k[k * B:(k + 1) * B], axis=1)).sum()) * n
+
+    span, _ = job_span(world, per_call)
+    if _SHARED:
+        pc_ev, pc_wall = [span], [span]
 
     # ---- cross-rank aggregation: sums of work, max of time (shard.py) --------
-    from paper_2001_07979_b200.shard import reduce_work_time
-
-    (good_bits_all, e2e_good_all, frames_all), (total_ms_max, e2e_ms_max) = reduce_work_time(
-        [float(good_bits), float(e2e_good * e2e_steps), float(B)], [total_ms, e2e_total_ms], device=dev)
-
-    value = good_bits_all / (total_ms_max / 1e3) / 1e6
-    e2e_value = e2e_good_all / (e2e_ms_max / 1e3) / 1e6
+    (good_all, e2e_good_all, pc_good_all, frames_all), (total_max, e2e_max, wall_max, pc_max, pcw_max) = \
+        reduce_work_time([float(gbits), float(e2e_good), float(pc_good), float(B)],
+                         [total_ms, e2e_ms, e2e_wall, sum(pc_ev), sum(pc_wall)], device=red_device(dev))
+    value = good_all / (total_max / 1e3) / 1e6
+    e2e_value = e2e_good_all / (e2e_max / 1e3) / 1e6
 
     # ---- roofline of the dominant kernel (the cooperative decode) ------------
     E = int(ens.matrices[0].edge_count) * u
-    per_frame = [alg_bytes_per_frame(n, m, u, E, int(i)) for i in iters]
-    alg_bytes = float(sum(per_frame))
+    alg_bytes = float(sum(alg_bytes_per_frame(n, m, u, E, int(i)) for i in iters))
     kms_mean = statistics.mean(kernel_ms)
     achieved = alg_bytes / (kms_mean / 1e3) / 1e9
     peak, peak_kind = measured_peak_hbm()
-    traffic = None
-    tf = ROOT / "profiles" / "decode_traffic.json"
-    if tf.exists():
-        try:
-            t = json.loads(tf.read_text())
-            if t.get("workload") == args.workload and t.get("frames") == B and t.get("e") == args.e:
-                traffic = t.get("dram_bytes_per_launch")
-        except Exception:
-            pass
-
-    # compute-side view: SFU (MUFU) operations of the check rule
+    trec = traffic_record(args.workload, B, args.e) if args.precision == "fp32" else None
+    traffic = trec.get("dram_bytes_per_launch") if trec else None
+    dram_frac = traffic / (kms_mean / 1e3) / 1e9 / peak if traffic else None
     mufu_ops = float(sum(rule_evals(i) for i in iters)) * E * MUFU_PER_EDGE
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
     clocks_summary = clocks.summary()
     sm_mhz = clocks_summary.get("sm_mhz") or 1965.0
     mufu_peak = MUFU_PER_CLK_SM * sm_count * sm_mhz * 1e6
     mufu_ach = mufu_ops / (kms_mean / 1e3)
+    hbm_bound = args.workload == "cfg4"
 
     line = {
         "metric": "reconciliation throughput (corrected Mbps)",
-        "value": round(value, 3), "unit": "Mbps", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(total_ms_max / args.steps, 4),
+        "value": round(value, 3), "unit": "Mbps", "n_gpus": world, "devices": devices, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(total_max / args.steps, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32" if args.precision == "fp32" else "f64",
-        "data": "synthetic (reference Philox frame streams, "
+        "data": "synthetic (the reference's Philox frame streams, generated on the GPU bit for bit; "
                 + ("synthetic random regular graphs)" if args.workload == "cfg4" else "PEG ensemble from the reference)"),
-        "config": config_dict(args, ens),
+        "config": config_dict(args, ens, world, devices),
+        "timing": ("host clock over the barrier-synchronised job span (ranks time-slice shared GPUs)" if _SHARED
+                   else "CUDA events on each rank's launching stream, max over ranks"),
         "fer": round(1.0 - float(conv.mean()), 6), "mean_iterations": round(float(iters.mean()), 4),
         "sweeps_run": sweeps,
         "e2e": {"value": round(e2e_value, 3), "unit": "Mbps",
-                "h2d_bytes_per_step": int(fb.noisy.nbytes + pin_syn.nbytes + 8),
-                "d2h_bytes_per_step": int(corrected.nbytes + 9 * B),
-                "timing": "CUDA events on the workspace stream around mbp_decode_batch (host pinned buffers)"},
-        "gpu_launches": 5 * args.steps,
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": "mbp::decode_scatter_kernel (cooperative, persistent, all sweeps)",
-                     "kernel_ms": round(kms_mean, 4), "alg_bytes_per_launch": alg_bytes,
-                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                     "note": "achieved = SURVEY 8(d) message-streaming bytes / kernel time; the scatter "
-                             "kernel keeps sweep-1/2 messages out of HBM, so frac > 1 is possible and "
-                             "`traffic` (ncu DRAM bytes) is the real traffic",
-                     "compute": {"unit": "MUFU op/s", "achieved": round(mufu_ach / 1e12, 4),
-                                 "peak": round(mufu_peak / 1e12, 4), "scale": "1e12",
-                                 "frac": round(mufu_ach / mufu_peak, 4),
-                                 "basis": f"{MUFU_PER_EDGE} SFU ops per edge per Eq. 6 evaluation, "
-                                          f"{MUFU_PER_CLK_SM}/clk/SM x {sm_count} SMs x median SM clock"}},
+                "h2d_bytes_per_step": int(B * (nb + pin_syn.a.shape[1]) + 8),
+                "d2h_bytes_per_step": int(B * (nb + 9)),
+                "host_wall_value": round(e2e_good_all / (wall_max / 1e3) / 1e6, 3),
+                "timing": f"one mbp_decode_batch host call over the {K} steps' batches ({K}x{B} frames per rank, "
+                          "pinned buffers): each step's H2D, decode and D2H overlap the neighbouring steps' "
+                          "(two-slot staging ring); CUDA events on the workspace stream, max over ranks; "
+                          "host_wall_value: perf_counter around the call",
+                "per_call": {"value": round(pc_good_all / (pc_max / 1e3) / 1e6, 3),
+                             "host_wall_value": round(pc_good_all / (pcw_max / 1e3) / 1e6, 3),
+                             "timing": f"{K} separate {B}-frame host calls (copies cannot overlap inside one)"}},
+        "gpu_launches": KERNELS_PER_DECODE * args.steps,
+        "roofline": {
+            "bound": "hbm" if hbm_bound else "latency",
+            "bound_detail": ("HBM: random 128-byte variable-block lines, L2 hit ~22 % (profiles/)" if hbm_bound else
+                             "L2/gather latency and issue (ncu: long-scoreboard stalls, ~50 % warps active, "
+                             "DRAM well below peak; profiles/r02*_scatter_ncu.md)"),
+            "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic,
+            "dram_frac": round(dram_frac, 4) if dram_frac is not None else None,
+            "traffic_source": (f"ncu --set full capture {trec.get('capture')} of these sources "
+                               f"(src {trec.get('src_sha')})" if trec else
+                               "no ncu capture of these sources committed (profiles/decode_traffic.json)"),
+            "kernel": "mbp::decode_scatter_kernel (cooperative, persistent, all sweeps)",
+            "kernel_ms": round(kms_mean, 4), "alg_bytes_per_launch": alg_bytes,
+            "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+            "note": "achieved = SURVEY 8(d) message-streaming bytes / kernel time (the scatter kernel keeps "
+                    "sweep-1/2 messages out of HBM, so frac > 1 is possible); dram_frac = ncu DRAM bytes / "
+                    "kernel time / peak is the real HBM utilisation",
+            "compute": {"unit": "MUFU op/s", "achieved": round(mufu_ach / 1e12, 4),
+                        "peak": round(mufu_peak / 1e12, 4), "scale": "1e12",
+                        "frac": round(mufu_ach / mufu_peak, 4),
+                        "basis": f"{MUFU_PER_EDGE} SFU ops per edge per Eq. 6 evaluation, "
+                                 f"{MUFU_PER_CLK_SM}/clk/SM x {sm_count} SMs x median SM clock"}},
         "clocks": clocks_summary,
     }
 
+    if args.stream:
+        line["stream"] = run_stream(args, ens, dec, rank, world, device, flush, stream)
+
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        corrected_c, conv_c, _, wall, frames_c, threads = cpu_decode_sample(ens, fb.noisy, pin_syn, args.e)
-        good_c = conv_c & np.all(corrected_c == fb.keys[:frames_c], axis=1)
+        corrected_c, conv_c, iters_c, mism_c, wall, frames_c, threads = cpu_decode_sample(
+            ens, noisy_d.cpu().numpy(), syn_d.cpu().numpy(), args.e)
+        good_c = conv_c & np.all(corrected_c == keys_h[:frames_c], axis=1)
         line["cpu_baseline"] = {"value": round(int(good_c.sum()) * n / wall / 1e6, 4), "unit": "Mbps",
-                                "cores": threads, "kind": "port",
+                                "cores": physical_cores(), "threads": threads, "kind": "port",
                                 "sample": f"first {frames_c} of the {B} frames, oracle/mbp_oracle.c "
-                                          f"(reference decode_loop restated in C/libm fp64) on {threads} threads, "
-                                          f"{wall:.1f} s wall"}
+                                          f"(reference decode_loop restated in C/libm fp64) on {threads} threads "
+                                          f"({physical_cores()} physical cores), {wall:.1f} s wall"}
+        bad = ((conv_c != conv[:frames_c]) | (iters_c != iters[:frames_c]) | (mism_c != mism[:frames_c])
+               | (conv_c & np.any(corrected_c != corrected[:frames_c], axis=1)))
+        line["parity"] = {"frames": int(frames_c), "mismatching_frames": int(bad.sum()),
+                          "checked": "per frame: converged, iterations, residual mismatches, corrected key of "
+                                     "converged frames -- GPU (this run) vs the oracle (reference decode_loop, "
+                                     "fp64) on the same frames"}
+    if rank == 0 and not args.no_extra and args.workload == "cfg2":
+        line["configs"] = {
+            "cfg3": side_config("cfg3", 0.03, "fp32", B, 10, device, flush, stream),
+            "cfg2_fp64": side_config("cfg2", args.e, "fp64", B, 5, device, flush, stream),
+        }
     if rank == 0 and not args.no_sweep:
         sweep = {}
         for e in (0.02, 0.04, 0.05):
-            _, fbe = load_workload(rank, B, e, world, args.workload)
-            syn_e = dec.syndromes(torch.from_numpy(fbe.keys).to(dev))
-            nd = torch.from_numpy(fbe.noisy).to(dev)
+            kq, nq, sq = device_frames(dec, n, e, lo, B, device)
             ed = torch.tensor([e], dtype=torch.float64, device=dev)
-            dec.decode_device(nd, syn_e, ed, out=out)
-            ts = []
-            for k in range(5):
-                flush.fill_(k)
-                s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                s0.record(stream)
-                dec.decode_device(nd, syn_e, ed, out=out)
-                s1.record(stream)
-                torch.cuda.synchronize(dev)
-                ts.append(s0.elapsed_time(s1))
-            ok = out[1].cpu().numpy().astype(bool) & np.all(out[0].cpu().numpy() == fbe.keys, axis=1)
-            sweep[str(e)] = {"mbps": round(int(ok.sum()) * n / (statistics.mean(ts) / 1e3) / 1e6, 1),
-                             "fer": round(1 - float(out[1].cpu().numpy().mean()), 6),
-                             "mean_iterations": round(float(out[2].cpu().numpy().mean()), 3)}
+            dec.decode_device(nq, sq, ed, out=out)
+            ts, _ = time_device_steps(dec, nq, sq, ed, out, 5, flush, stream)
+            sweep[str(e)] = {"mbps": round(good_bits(out, kq, n) / (statistics.mean(ts) / 1e3) / 1e6, 1),
+                             "fer": round(1 - float(out[1].float().mean().item()), 6),
+                             "mean_iterations": round(float(out[2].float().mean().item()), 3)}
         line["qber_sweep"] = sweep
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
-        torch.distributed.destroy_process_group()
+        dist.barrier()
+        dist.destroy_process_group()
     return 0
 
 

@@ -50,6 +50,19 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found; the CUDA toolkit is required to build libmbp_b200.so")
 
 
+def source_hash() -> str:
+    """SHA-256 (16 hex) over the library's sources and build flags: keys
+    measurements (ncu DRAM traffic, profiles/decode_traffic.json) to the code
+    they were taken on."""
+    import hashlib
+
+    h = hashlib.sha256(" ".join(NVCC_FLAGS[:-2]).encode())
+    for p in DEPS:
+        h.update(p.name.encode())
+        h.update(p.read_bytes())
+    return h.hexdigest()[:16]
+
+
 def stale() -> bool:
     if not LIB.exists():
         return True

@@ -132,8 +132,14 @@ struct mbp_workspace {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
     int last_B = 0;
     bool timed = false, e2e_timed = false;
+    // pinned staging of the host path's crossover probabilities: an async
+    // copy from pageable memory would block the issuing thread until the
+    // copy stream drains, serialising the staging ring
+    double* e_host = nullptr;
+    size_t e_host_cap = 0;
     ~mbp_workspace()
     {
+        if (e_host) cudaFreeHost(e_host);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         if (ev2) cudaEventDestroy(ev2);
@@ -753,6 +759,25 @@ static int host_subbatches(const mbp_workspace* ws, int64_t batch)
     return (int)std::max<int64_t>(1, std::min<int64_t>(mbp_workspace::kMaxSub, batch / 1024));
 }
 
+// e (1 or batch values) copied into the workspace's pinned staging buffer
+static int stage_e(mbp_workspace* ws, const double* e, size_t ne, const double** staged)
+{
+    if (ws->e_host_cap < ne) {
+        // the previous staging may still feed an in-flight copy of this workspace
+        MBP_CUDA(cudaStreamSynchronize(ws->h2d_stream));
+        if (ws->e_host) cudaFreeHost(ws->e_host);
+        ws->e_host = nullptr;
+        ws->e_host_cap = 0;
+        MBP_CUDA(cudaHostAlloc((void**)&ws->e_host, std::max<size_t>(ne, 1024) * 8, cudaHostAllocPortable));
+        ws->e_host_cap = std::max<size_t>(ne, 1024);
+    } else {
+        MBP_CUDA(cudaStreamSynchronize(ws->h2d_stream));
+    }
+    std::memcpy(ws->e_host, e, ne * 8);
+    *staged = ws->e_host;
+    return MBP_OK;
+}
+
 static int decode_host_stream(mbp_workspace* ws, const uint8_t* noisy, const uint8_t* syn, const double* e,
                               int32_t e_stride, int64_t batch, uint8_t* corrected, uint8_t* converged,
                               int32_t* iterations, int32_t* mismatches)
@@ -767,6 +792,7 @@ static int decode_host_stream(mbp_workspace* ws, const uint8_t* noisy, const uin
         (rc = ensure(ws->tmp_conv, 2 * cap)) || (rc = ensure(ws->tmp_iters, 2 * cap * 4)) ||
         (rc = ensure(ws->tmp_mism, 2 * cap * 4)) || (rc = ensure(ws->tmp_e, 2 * ne * 8)))
         return rc;
+    if ((rc = stage_e(ws, e, e_stride ? (size_t)batch : 1, &e))) return rc;
     MBP_CUDA(cudaEventRecord(ws->ev2, s));
     MBP_CUDA(cudaStreamWaitEvent(ws->h2d_stream, ws->ev2, 0));
     MBP_CUDA(cudaStreamWaitEvent(ws->d2h_stream, ws->ev2, 0));
@@ -830,6 +856,7 @@ int mbp_decode_batch(mbp_workspace* ws, const uint8_t* noisy, const uint8_t* syn
         (rc = ensure(ws->tmp_conv, batch)) || (rc = ensure(ws->tmp_iters, batch * 4)) ||
         (rc = ensure(ws->tmp_mism, batch * 4)) || (rc = ensure(ws->tmp_e, ne * 8)))
         return rc;
+    if ((rc = stage_e(ws, e, ne, &e))) return rc;
     uint8_t* d_noisy = ws->tmp_in.as<uint8_t>();
     uint8_t* d_syn = d_noisy + batch * nb;
     const int nsub = host_subbatches(ws, batch);

@@ -238,10 +238,21 @@ class BatchDecoder:
         if out is None:
             out = BatchResult(np.empty_like(noisy), np.empty(B, dtype=np.uint8),
                               np.empty(B, dtype=np.int32), np.empty(B, dtype=np.int32), self.dev.n)
+        else:   # caller-owned (e.g. pinned) buffers are written in place
+            for a, nm, dts, shp in ((out.corrected, "corrected", (np.uint8,), noisy.shape),
+                                    (out.converged, "converged", (np.uint8, np.bool_), (B,)),
+                                    (out.iterations, "iterations", (np.int32,), (B,)),
+                                    (out.mismatches, "mismatches", (np.int32,), (B,))):
+                if (not isinstance(a, np.ndarray) or a.dtype.type not in dts or a.shape[:len(shp)] != tuple(shp)
+                        or a.shape[0] != shp[0] or not a.flags.c_contiguous or not a.flags.writeable):
+                    raise ValueError(f"out.{nm} must be a writeable contiguous {dts[0].__name__} array of "
+                                     f"shape {tuple(shp)}")
         N.call("mbp_decode_batch", self.handle, noisy.ctypes.data, syn.ctypes.data, ev.ctypes.data,
                0 if ev.size == 1 else 1, B, N.ptr(out.corrected), N.ptr(out.converged),
                N.ptr(out.iterations), N.ptr(out.mismatches))
-        out.converged = out.converged.astype(bool)
+        # a bool VIEW of the same (possibly pinned) bytes: the buffer stays the
+        # caller's, so a reused `out` keeps copying into pinned memory
+        out.converged = out.converged.view(np.bool_)
         return out
 
     def _check_device_tensor(self, t, name, dtype, shape=None):

@@ -62,6 +62,7 @@ def main():
     ap.add_argument("--frames", type=int, default=1024)
     ap.add_argument("--e", type=float, default=0.03)
     ap.add_argument("--title", default="decode_kernel")
+    ap.add_argument("--workload", default="cfg2")
     a = ap.parse_args()
     m = raw(a.rep)
     lines = [f"# ncu summary: {a.title}", "", f"report: `{a.rep}` (ncu --set full --clock-control none)", "",
@@ -88,11 +89,27 @@ def main():
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(u, 1)
         return v * scale
     if a.traffic_json and "dram__bytes_read.sum" in m:
-        t = {"workload": "cfg2", "frames": a.frames, "e": a.e,
+        # one record per (workload, frames, e), keyed to the library sources
+        # the capture ran on (bench.py drops `traffic` for other sources)
+        import sys
+        from pathlib import Path
+
+        sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+        from paper_2001_07979_b200.build import source_hash
+
+        t = {"workload": a.workload, "frames": a.frames, "e": a.e, "src_sha": source_hash(),
              "dram_bytes_per_launch": num("dram__bytes_read.sum") + num("dram__bytes_write.sum"),
              "dram_read": num("dram__bytes_read.sum"), "dram_write": num("dram__bytes_write.sum"),
-             "source": a.rep}
-        open(a.traffic_json, "w").write(json.dumps(t, indent=1) + "\n")
+             "kernel_ms_ncu": num("gpu__time_duration.sum") / (1e6 if m["gpu__time_duration.sum"][1] == "ns" else 1e3
+                                                               if m["gpu__time_duration.sum"][1] == "us" else 1),
+             "capture": Path(a.rep).name, "summary": a.out}
+        try:
+            old = json.loads(open(a.traffic_json).read())
+            old = old if isinstance(old, list) else [old]
+        except (OSError, ValueError):
+            old = []
+        keep = [r for r in old if (r.get("workload"), r.get("frames"), r.get("e")) != (a.workload, a.frames, a.e)]
+        open(a.traffic_json, "w").write(json.dumps(keep + [t], indent=1) + "\n")
     print("\n".join(lines[:30]))
 
 
