@@ -29,6 +29,7 @@ UNITS = [
     ("mbp", "mbp.cu", []),
     ("peg", "peg.cpp", []),
     ("frames", "frames.cu", []),
+    ("peg_gpu", "peg_gpu.cu", []),
     ("k_explicit_f32", "k_explicit.cu", []),
     ("k_explicit_f64", "k_explicit.cu", ["-DMBP_EXPLICIT_F64=1"]),
     ("k_explicit_f64w", "k_explicit.cu", ["-DMBP_EXPLICIT_F64=2"]),
@@ -81,9 +82,18 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False, 
     obj_dir.mkdir(parents=True, exist_ok=True)
     cc = nvcc()
 
+    headers = sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [ROOT / "include" / "mbp.h"]
+    flags_file = obj_dir / "flags.txt"
+    flags_now = " ".join([*NVCC_FLAGS, *[f"-D{d}" for d in defines], str(ptxas_info)])
+    same_flags = flags_file.exists() and flags_file.read_text() == flags_now
+
     def compile_unit(unit):
         name, src, defs = unit
         obj = obj_dir / f"{name}.o"
+        if not force and same_flags and obj.exists():
+            t = obj.stat().st_mtime
+            if all(p.stat().st_mtime <= t for p in [CSRC / src, *headers]):
+                return obj   # up to date: sources and headers older than the object
         cmd = [cc, *NVCC_FLAGS, *defs, *[f"-D{d}" for d in defines], *(["-Xptxas", "-v"] if ptxas_info else []),
                "-c", "-o", str(obj),
                str(CSRC / src)]
@@ -98,6 +108,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False, 
 
     with ThreadPoolExecutor(max_workers=len(UNITS)) as pool:
         objs = list(pool.map(compile_unit, UNITS))
+    flags_file.write_text(flags_now)
     tmp = lib.with_suffix(".so.tmp")
     cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
     if verbose:

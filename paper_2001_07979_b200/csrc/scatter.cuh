@@ -155,6 +155,22 @@ struct SL {
     __device__ __forceinline__ int Lfix(int s) const { return ld_cg((CPT ? A.Lfix_b : A.Lfix) + s); }
 };
 
+// round(c * scale) for a message |c| <= clamp.  With MBP_FIX_MAGIC the
+// conversion runs on the FMA pipe (c * 2^S + 1.5 * 2^23 rounds to the nearest
+// integer, ties to even, when |c * 2^S| < 2^22 -- the kernel caps S for
+// that) instead of F2I, which issues on the XU pipe next to the rule's MUFUs.
+#ifndef MBP_FIX_MAGIC
+#define MBP_FIX_MAGIC 0
+#endif
+__device__ __forceinline__ int fixq(float c, float scale)
+{
+#if MBP_FIX_MAGIC
+    return __float_as_int(fmaf(c, scale, 12582912.0f)) - 0x4B400000;
+#else
+    return __float2int_rn(c * scale);
+#endif
+}
+
 __device__ __forceinline__ const float* byte_off(const float* p, unsigned off)
 {
     return reinterpret_cast<const float*>(reinterpret_cast<const char*>(p) + off);
@@ -257,12 +273,12 @@ __device__ __forceinline__ void sc_row(const ScatterArgs& A, const SL<CPT>& S, c
     // differences c2v'_t - c2v'_{t-1} leaves prior + sum of c2v'_t exactly
     int vold[DD];
     if (t == 2) {
-        const int v1 = __float2int_rn(c[0] * scale);   // row constant
+        const int v1 = fixq(c[0], scale);   // row constant
 #pragma unroll
         for (int k = 0; k < DD; ++k) vold[k] = v1;
     } else if (explicit_base) {
 #pragma unroll
-        for (int k = 0; k < DD; ++k) vold[k] = __float2int_rn(c[k] * scale);
+        for (int k = 0; k < DD; ++k) vold[k] = fixq(c[k], scale);
     }
     rule_sd<DD, PAD, SAT>(x, d, sj, A.clamp, A.sat, c);
     if (t > 2 && !explicit_base) {
@@ -279,7 +295,7 @@ __device__ __forceinline__ void sc_row(const ScatterArgs& A, const SL<CPT>& S, c
                     pv = ld_cg(q);
                 }
                 x[k] = pv - c[k];
-                if (s == t) vold[k] = __float2int_rn(c[k] * scale);
+                if (s == t) vold[k] = fixq(c[k], scale);
             }
             rule_sd<DD, PAD, SAT>(x, d, sj, A.clamp, A.sat, c);
         }
@@ -292,7 +308,7 @@ __device__ __forceinline__ void sc_row(const ScatterArgs& A, const SL<CPT>& S, c
     }
 #pragma unroll
     for (int k = 0; k < DD; ++k) {
-        const int v = __float2int_rn(c[k] * scale) - (CPT && absolute ? 0 : vold[k]);
+        const int v = fixq(c[k], scale) - (CPT && absolute ? 0 : vold[k]);
         red_add(byte_off(gb, soff[k]) + 64, (!PAD || k < d) ? v : 0);   // acc line
     }
 }
@@ -929,7 +945,14 @@ __global__ void __launch_bounds__(kDecodeThreads, scatter_min_blocks<D>()) decod
     // fixed-point scale: |acc| <= Lmax + dv_max * clamp (+ rounding) < 2^30
     int ex;
     frexpf(ld_cg(A.Lmax) + (float)A.dv_max * A.clamp + 2.0f, &ex);
-    const int S = min(30 - ex, 40);
+    int S = min(30 - ex, 40);
+#if MBP_FIX_MAGIC
+    {   // fixq's range: |message| * 2^S < 2^22
+        int ec;
+        frexpf(A.clamp, &ec);
+        S = min(S, 22 - ec);
+    }
+#endif
     const float scale = ldexpf(1.0f, S), iscale = ldexpf(1.0f, -S);
 
     bool cpt = false;

@@ -174,14 +174,16 @@ class MatrixEnsemble:
         return [h.content_hash() for h in self.matrices]
 
 
-def peg_construct(n: int, m: int, column_degree=3, seed: int = 0) -> ParityCheckMatrix:
+def peg_construct(n: int, m: int, column_degree=3, seed: int = 0, device: int | None = None) -> ParityCheckMatrix:
     """Progressive-edge-growth matrix, identical to the reference's
     ``matrix.peg_construct(n, m, DegreeProfile, seed)`` (matrix.py:215-234)
     for the same seed: ``mbp_peg_build`` in the native library restates
     ``_kernels.peg_build`` (BFS order, candidate scan, xorshift64* ties).
     ``column_degree``: an int (regular) or n per-column degrees (>= 2, as
-    DegreeProfile requires).  Sequential host code: seconds at n = 2^16,
-    hours at 2^20 (the reference's cost grows the same way, ~n*m)."""
+    DegreeProfile requires).  Host code is sequential: seconds at n = 2^16,
+    hours at 2^20 (the reference's cost grows the same way, ~n*m).
+    ``device``: run each edge's BFS on that GPU (mbp_peg_build_device, the
+    same matrix; the practical route at n = 2^20)."""
     import ctypes as C
 
     from . import _native as N
@@ -203,13 +205,17 @@ def peg_construct(n: int, m: int, column_degree=3, seed: int = 0) -> ParityCheck
     E = int(deg.sum())
     chk_ptr = np.zeros(m + 1, dtype=np.int64)
     chk_var = np.zeros(E, dtype=np.int32)
-    N.call("mbp_peg_build", int(n), int(m), deg.ctypes.data, C.c_uint64(int(seed) & 0xFFFFFFFFFFFFFFFF),
-           chk_ptr.ctypes.data, chk_var.ctypes.data)
+    if device is None:
+        N.call("mbp_peg_build", int(n), int(m), deg.ctypes.data, C.c_uint64(int(seed) & 0xFFFFFFFFFFFFFFFF),
+               chk_ptr.ctypes.data, chk_var.ctypes.data)
+    else:
+        N.call("mbp_peg_build_device", int(n), int(m), deg.ctypes.data,
+               C.c_uint64(int(seed) & 0xFFFFFFFFFFFFFFFF), chk_ptr.ctypes.data, chk_var.ctypes.data, int(device))
     return ParityCheckMatrix._from_csr(n, m, chk_ptr, chk_var)
 
 
 def build_ensemble(n: int, m: int, column_degree=3, u: int = 1, base_seed: int = 0,
-                   workers: int | None = None) -> "MatrixEnsemble":
+                   workers: int | None = None, device: int | None = None) -> "MatrixEnsemble":
     """u PEG matrices from seeds base_seed..base_seed+u-1, as the reference's
     ``build_ensemble`` (matrix.py:237-256); members build in parallel
     threads (the native call releases the GIL)."""
@@ -217,12 +223,12 @@ def build_ensemble(n: int, m: int, column_degree=3, u: int = 1, base_seed: int =
         raise ValueError(f"u must be >= 1, got {u}")
     seeds = [base_seed + k for k in range(u)]
     if u == 1 or (workers is not None and workers <= 1):
-        mats = [peg_construct(n, m, column_degree, s) for s in seeds]
+        mats = [peg_construct(n, m, column_degree, s, device) for s in seeds]
     else:
         from concurrent.futures import ThreadPoolExecutor
 
         with ThreadPoolExecutor(max_workers=workers or min(u, 4)) as pool:
-            mats = list(pool.map(lambda s: peg_construct(n, m, column_degree, s), seeds))
+            mats = list(pool.map(lambda s: peg_construct(n, m, column_degree, s, device), seeds))
     return MatrixEnsemble(tuple(mats))
 
 

@@ -26,13 +26,16 @@ SPECS = {
     "cfg1": (4096, 2048, 2, 1),
     "cfg2": (65536, 32768, 2, 1),
     "cfg3": (65536, 14650, 3, 11),
+    "cfg4": (1 << 20, 1 << 19, 2, 1),   # BASELINE configs[3]: ~7 h per matrix in the reference
     "mid": (512, 256, 3, 91),      # reference tests/conftest.py:17-20
     "toy": (64, 32, 3, 41),        # reference tests/conftest.py:11-14
     "desk": (16384, 8192, 3, 1001),  # reference test_acceptance.py:53-59
 }
 
 if __name__ == "__main__":
-    out = ROOT / "paper_2001_07979_b200" / "ensembles"
+    import os
+
+    out = Path(os.environ.get("ENSEMBLE_OUT", ROOT / "paper_2001_07979_b200" / "ensembles"))
     out.mkdir(parents=True, exist_ok=True)
     for name in sys.argv[1:]:
         n, m, u, seed = SPECS[name]

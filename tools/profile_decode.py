@@ -16,7 +16,7 @@ sys.path.insert(0, str(ROOT))
 
 from paper_2001_07979_b200 import BatchDecoder, DecoderConfig  # noqa: E402
 from paper_2001_07979_b200 import _native as N  # noqa: E402
-from paper_2001_07979_b200.channel import make_frames  # noqa: E402
+from paper_2001_07979_b200.channel import make_frames_native as make_frames  # noqa: E402
 from paper_2001_07979_b200.matrix import load_ensemble  # noqa: E402
 
 
