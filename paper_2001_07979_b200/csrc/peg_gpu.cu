@@ -49,7 +49,7 @@ constexpr int KC = 16;         // check adjacency capacity (PEG keeps rows near 
 constexpr int PB = 512;        // threads per block
 constexpr int INF = 1 << 30;
 constexpr int ND = KC + 1;     // candidate degrees 0..KC
-constexpr long long kSmallLevel = 32768;  // items block 0 expands alone
+constexpr long long kSmallLevel = 8192;   // slots block 0 expands alone
 
 struct PegSummary {
     int mode;                  // 0: unreached checks in index order, 1: deepest level in BFS order
@@ -72,9 +72,12 @@ struct PegArgs {
     int* vis_v;                // [n]
     unsigned long long* key_c; // [m] (~token << 32 | discovery slot)
     unsigned long long* key_v; // [n]
-    int* lvl;                  // [m] current check level (ordered)
-    int* fr;                   // [n] current variable frontier (ordered)
-    int* blk;                  // [grid] per-block counts (compaction)
+    int* lvl;                  // current check level: block regions (see Level)
+    int* fr;                   // current variable frontier: block regions
+    int* lvl_cnt;              // [grid] discoverers per block region
+    int* fr_cnt;               // [grid]
+    long long* lvl_seg;        // region stride of lvl
+    long long* fr_seg;         // region stride of fr
     int* blk_k;                // [grid] per-block dmin counts after p0 (kept for the next attach)
     int* blk_min;              // [grid] per-block candidate minimum (summary)
     int* st_cnt;               // [grid][ND] candidates per degree (summary)
@@ -158,57 +161,47 @@ __device__ __forceinline__ int block_excl_min(int x, int* sh, int* bmin)
     return r;
 }
 
-// sum over blocks [0, b) and [0, grid) of blk[]
-__device__ __forceinline__ void blk_prefix(const int* blk, int b, int* sh, int* before, int* total)
-{
-    int a = 0, t = 0;
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += PB) {
-        const int x = ld_cg(blk + i);
-        t += x;
-        if (i < b) a += x;
-    }
-    int tot;
-    block_excl_sum(a, sh, &tot);
-    *before = tot;
-    block_excl_sum(t, sh, &tot);
-    *total = tot;
-}
-
-// Ordered compaction of the discoverers among `items` slots: slot i is a
-// discoverer of node x(i) when key[x] == mk(token, i).  Writes the nodes in
-// slot order to out[] and stamps vis[x] = token; returns the count (on every
-// thread).  Each block owns one contiguous slot segment.
-template <class Node>
-__device__ __forceinline__ int compact(const PegArgs& A, long long items, int token, int hl, Node node,
-                                       const unsigned long long* key, int* vis, int* out, int* sh)
-{
-    const long long seg = (items + gridDim.x - 1) / gridDim.x;
-    const long long s0 = min(items, (long long)blockIdx.x * seg), s1 = min(items, s0 + seg);
-    int cnt = 0;
-    for (long long c0 = s0; c0 < s1; c0 += PB) {
-        const long long i = c0 + threadIdx.x;
-        int x = -1;
-        const bool d = i < s1 && (x = node(i)) >= 0 && ld_cg(key + x) == mk(token, hl, i);
-        cnt += __syncthreads_count(d);
-    }
-    if (threadIdx.x == 0) A.blk[blockIdx.x] = cnt;
-    grid_barrier(A.bar);
-    int before, total;
-    blk_prefix(A.blk, blockIdx.x, sh, &before, &total);
-    int pos = before;
-    for (long long c0 = s0; c0 < s1; c0 += PB) {
-        const long long i = c0 + threadIdx.x;
-        int x = -1;
-        const bool d = i < s1 && (x = node(i)) >= 0 && ld_cg(key + x) == mk(token, hl, i);
-        int tot;
-        const int r = block_excl_sum(d ? 1 : 0, sh, &tot);
-        if (d) {
-            out[pos + r] = x;
-            vis[x] = token;
+// A BFS level as the grid leaves it: block b's discoverers, in order, at
+// buf[b * seg ...], cnt[b] of them; the level's global order is block-major.
+// pre[] (shared, grid+1 entries) holds the prefix counts.  Callers walk a
+// level in tiles of consecutive positions: tile() finds the tile's first
+// region once (binary search, one thread), at() steps forward from it.
+struct Level {
+    const int* buf;
+    long long seg;
+    const int* pre;   // shared
+    int* hint;        // shared: region of the current tile's first position
+    int total;
+    __device__ __forceinline__ void tile(long long q0) const   // all threads; ends with __syncthreads
+    {
+        if (threadIdx.x == 0) {
+            int lo = 0, hi = gridDim.x;
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (pre[mid] <= q0) lo = mid; else hi = mid;
+            }
+            *hint = lo;
         }
-        pos += tot;
+        __syncthreads();
     }
-    return total;
+    __device__ __forceinline__ int at(long long q) const
+    {
+        int r = *hint;
+        while (r + 1 < (int)gridDim.x && pre[r + 1] <= q) ++r;
+        return ld_cg(buf + (long long)r * seg + (q - pre[r]));
+    }
+};
+
+// load a level descriptor's prefix table into shared memory (all threads)
+__device__ __forceinline__ int load_prefix(const int* cnt, int* pre, int* sh)
+{
+    const int x = threadIdx.x < (int)gridDim.x ? ld_cg(cnt + threadIdx.x) : 0;
+    int tot;
+    const int e = block_excl_sum(x, sh, &tot);
+    if (threadIdx.x < (int)gridDim.x) pre[threadIdx.x] = e;
+    if (threadIdx.x == 0) pre[gridDim.x] = tot;
+    __syncthreads();
+    return tot;
 }
 
 // Attach check c to variable v (one thread).
@@ -225,49 +218,76 @@ __device__ __forceinline__ void attach(const PegArgs& A, int c, int v)
     A.sum->winner = c;
 }
 
-// Block-local ordered compaction (the small levels that block 0 runs alone).
-template <class Node>
-__device__ __forceinline__ int compact_block(long long items, int token, int hl, Node node,
-                                             const unsigned long long* key, int* vis, int* out, int* sh)
+// One expansion of the BFS: the slots i = q * K + k of level `from` (q its
+// position, k < K an adjacency slot) discover the unvisited nodes they point
+// to; the first slot in order wins (atomicMin of the key), as in the
+// reference's sequential walk.  Blocks own contiguous slot segments and
+// write their discoverers, in slot order, to out[b * seg ...]; out_cnt[b]
+// gets the count.  `grid_mode` false: block 0 alone (small levels).
+template <class Nbr>
+__device__ __forceinline__ void expand(const PegArgs& A, int token, int hl, const Level& from, int K, Nbr nbr,
+                                       unsigned long long* key, int* vis, int* out, int* out_cnt,
+                                       long long* out_seg, bool grid_mode, int* sh)
 {
+    const long long items = (long long)from.total * K;
+    const int nb = grid_mode ? gridDim.x : 1;
+    const int bid = grid_mode ? blockIdx.x : 0;
+    const long long seg = (items + nb - 1) / nb;
+    const long long s0 = min(items, (long long)bid * seg), s1 = min(items, s0 + seg);
+    for (long long c0 = s0; c0 < s1; c0 += PB) {
+        from.tile(c0 / K);
+        const long long i = c0 + threadIdx.x;
+        if (i < s1) {
+            const int x = nbr(from.at(i / K), (int)(i % K));
+            if (x >= 0 && ld_cg(vis + x) != token) atomicMin(key + x, mk(token, hl, i));
+        }
+        __syncthreads();
+    }
+    if (grid_mode) grid_barrier(A.bar); else __syncthreads();
     int pos = 0;
-    for (long long c0 = 0; c0 < items; c0 += PB) {
+    for (long long c0 = s0; c0 < s1; c0 += PB) {
+        from.tile(c0 / K);
         const long long i = c0 + threadIdx.x;
         int x = -1;
-        const bool d = i < items && (x = node(i)) >= 0 && ld_cg(key + x) == mk(token, hl, i);
+        const bool d = i < s1 && (x = nbr(from.at(i / K), (int)(i % K))) >= 0 && ld_cg(key + x) == mk(token, hl, i);
         int tot;
         const int r = block_excl_sum(d ? 1 : 0, sh, &tot);
         if (d) {
-            out[pos + r] = x;
+            out[(long long)bid * seg + pos + r] = x;
             vis[x] = token;
         }
         pos += tot;
     }
-    return pos;
+    if (threadIdx.x == 0) out_cnt[bid] = pos;
+    if (!grid_mode) {
+        for (int b = 1 + threadIdx.x; b < (int)gridDim.x; b += PB) out_cnt[b] = 0;
+    }
+    if (bid == 0 && threadIdx.x == 0) *out_seg = seg;
+    if (grid_mode) grid_barrier(A.bar); else __syncthreads();
 }
 
 // One edge, one cooperative launch:
 //  1. block 0 attaches the previous edge's winner (it owns the candidate
-//     sequence the previous summary left: lvl / vis_c) and runs the BFS from
-//     v while its levels are small (block barriers only);
-//  2. the whole grid takes over for the large levels (grid barriers);
+//     sequence the previous summary left) and runs the BFS from v while its
+//     levels are small (block barriers only);
+//  2. the whole grid takes over for the large levels (two grid barriers per
+//     expansion);
 //  3. the candidate-scan summary: per-block degree histograms and first
 //     positions, one grid barrier, then dmin, p0, K* and the running-minimum
 //     ties before p0.
 __global__ void __launch_bounds__(PB) peg_step_kernel(PegArgs A, int v, int token, int attach_v,
-                                                      unsigned long long attach_j, int do_bfs)
+                                                      unsigned long long attach_j, int do_bfs, int kc)
 {
     __shared__ int sh[72];
     __shared__ int s_i[2 * ND + 4];
-    const int gtid = blockIdx.x * PB + threadIdx.x;
-    const int nthreads = gridDim.x * PB;
+    __shared__ int s_pre[PB + 1];
+    __shared__ int s_hint;
     const int m = A.m;
-    auto node_v2c = [&](long long i) {
-        const int w = ld_cg(A.fr + i / KV), k = (int)(i % KV);
+    Level F{A.fr, 0, s_pre, &s_hint, 0}, L{A.lvl, 0, s_pre, &s_hint, 0};
+    auto nbr_v2c = [&](int w, int k) {
         return k < ld_cg(A.vn_deg + w) ? ld_cg(A.vn_adj + (size_t)w * KV + k) : -1;
     };
-    auto node_c2v = [&](long long i) {
-        const int c = ld_cg(A.lvl + i / KC), k = (int)(i % KC);
+    auto nbr_c2v = [&](int c, int k) {
         return k < ld_cg(A.cn_deg + c) ? ld_cg(A.cn_adj + (size_t)c * KC + k) : -1;
     };
 
@@ -275,8 +295,13 @@ __global__ void __launch_bounds__(PB) peg_step_kernel(PegArgs A, int v, int toke
         // ---- 1a. attach the previous edge's winner ---------------------------
         if (attach_v >= 0) {
             const PegSummary S = *A.sum;
+            if (S.mode == 1) {
+                L.seg = ld_cg(A.lvl_seg);
+                L.total = load_prefix(A.lvl_cnt, s_pre, sh);
+            }
             if (attach_j == 0) {
-                if (threadIdx.x == 0) attach(A, S.mode == 0 ? S.p0 : ld_cg(A.lvl + S.p0), attach_v);
+                if (S.mode == 1) L.tile(S.p0);
+                if (threadIdx.x == 0) attach(A, S.mode == 0 ? S.p0 : L.at(S.p0), attach_v);
             } else {
                 // owner segment of the attach_j-th degree-dmin candidate after p0
                 const int cnt = threadIdx.x < (int)gridDim.x ? ld_cg(A.blk_k + threadIdx.x) : 0;
@@ -293,11 +318,12 @@ __global__ void __launch_bounds__(PB) peg_step_kernel(PegArgs A, int v, int toke
                 const long long s1 = min((long long)S.count, s0 + seg);
                 int pos = s_i[1];
                 for (long long c0 = s0; c0 < s1; c0 += PB) {
+                    if (S.mode == 1) L.tile(c0);
                     const long long i = c0 + threadIdx.x;
                     bool q = false;
                     int c = -1;
                     if (i < s1 && i > S.p0) {
-                        c = S.mode == 0 ? (int)i : ld_cg(A.lvl + i);
+                        c = S.mode == 0 ? (int)i : L.at(i);
                         q = (S.mode == 1 || ld_cg(A.vis_c + c) != token - 1) && ld_cg(A.cn_deg + c) == S.dmin;
                     }
                     const int r = block_excl_sum(q ? 1 : 0, sh, &tot);
@@ -312,34 +338,33 @@ __global__ void __launch_bounds__(PB) peg_step_kernel(PegArgs A, int v, int toke
             if (threadIdx.x == 0) {
                 A.vis_v[v] = token;
                 A.fr[0] = v;
+                A.fr_cnt[0] = 1;
+                *A.fr_seg = 1;
                 A.sum->t_pre = 0;
             }
+            for (int b = 1 + threadIdx.x; b < (int)gridDim.x; b += PB) A.fr_cnt[b] = 0;
             __syncthreads();
             int nF = 1, nL = 0, reached = 0, hl = 0, stage = 0, done = 0;
             for (;;) {
                 if (stage == 0) {
                     const long long items = (long long)nF * KV;
                     if (items > kSmallLevel) break;
-                    for (long long i = threadIdx.x; i < items; i += PB) {
-                        const int c = node_v2c(i);
-                        if (c >= 0 && ld_cg(A.vis_c + c) != token) atomicMin(A.key_c + c, mk(token, hl, i));
-                    }
-                    __syncthreads();
-                    nL = compact_block(items, token, hl, node_v2c, A.key_c, A.vis_c, A.lvl, sh);
+                    F.seg = ld_cg(A.fr_seg);
+                    F.total = load_prefix(A.fr_cnt, s_pre, sh);
+                    expand(A, token, hl, F, KV, nbr_v2c, A.key_c, A.vis_c, A.lvl, A.lvl_cnt, A.lvl_seg, false, sh);
+                    nL = ld_cg(A.lvl_cnt);
                     ++hl;
                     if (nL == 0) { done = 1; break; }
                     reached += nL;
                     if (reached == m) { done = 1; break; }
                     stage = 1;
                 } else {
-                    const long long items = (long long)nL * KC;
+                    const long long items = (long long)nL * kc;
                     if (items > kSmallLevel) break;
-                    for (long long i = threadIdx.x; i < items; i += PB) {
-                        const int w = node_c2v(i);
-                        if (w >= 0 && ld_cg(A.vis_v + w) != token) atomicMin(A.key_v + w, mk(token, hl, i));
-                    }
-                    __syncthreads();
-                    nF = compact_block(items, token, hl, node_c2v, A.key_v, A.vis_v, A.fr, sh);
+                    L.seg = ld_cg(A.lvl_seg);
+                    L.total = load_prefix(A.lvl_cnt, s_pre, sh);
+                    expand(A, token, hl, L, kc, nbr_c2v, A.key_v, A.vis_v, A.fr, A.fr_cnt, A.fr_seg, false, sh);
+                    nF = ld_cg(A.fr_cnt);
                     ++hl;
                     if (nF == 0) { done = 1; break; }
                     stage = 0;
@@ -360,44 +385,40 @@ __global__ void __launch_bounds__(PB) peg_step_kernel(PegArgs A, int v, int toke
     bool done = ld_cg(A.bfs + 5) != 0;
     while (!done) {
         if (stage == 0) {
-            const long long items = (long long)nF * KV;
-            for (long long i = gtid; i < items; i += nthreads) {
-                const int c = node_v2c(i);
-                if (c >= 0 && ld_cg(A.vis_c + c) != token) atomicMin(A.key_c + c, mk(token, hl, i));
-            }
-            grid_barrier(A.bar);
-            nL = compact(A, items, token, hl, node_v2c, A.key_c, A.vis_c, A.lvl, sh);
+            F.seg = ld_cg(A.fr_seg);
+            F.total = load_prefix(A.fr_cnt, s_pre, sh);
+            expand(A, token, hl, F, KV, nbr_v2c, A.key_c, A.vis_c, A.lvl, A.lvl_cnt, A.lvl_seg, true, sh);
+            nL = load_prefix(A.lvl_cnt, s_pre, sh);
             ++hl;
-            grid_barrier(A.bar);
             if (nL == 0) break;           // saturation
             reached += nL;
             if (reached == m) break;      // everything reachable: this level is the deepest
             stage = 1;
         } else {
-            const long long items = (long long)nL * KC;
-            for (long long i = gtid; i < items; i += nthreads) {
-                const int w = node_c2v(i);
-                if (w >= 0 && ld_cg(A.vis_v + w) != token) atomicMin(A.key_v + w, mk(token, hl, i));
-            }
-            grid_barrier(A.bar);
-            nF = compact(A, items, token, hl, node_c2v, A.key_v, A.vis_v, A.fr, sh);
+            L.seg = ld_cg(A.lvl_seg);
+            L.total = load_prefix(A.lvl_cnt, s_pre, sh);
+            expand(A, token, hl, L, kc, nbr_c2v, A.key_v, A.vis_v, A.fr, A.fr_cnt, A.fr_seg, true, sh);
+            nF = load_prefix(A.fr_cnt, s_pre, sh);
             ++hl;
-            grid_barrier(A.bar);
             if (nF == 0) break;
             stage = 0;
         }
         if (hl >= 1022) {
-            if (gtid == 0) A.sum->overflow = 1;
+            if (blockIdx.x == 0 && threadIdx.x == 0) A.sum->overflow = 1;
             break;
         }
     }
 
     // ---- 3. candidate-scan summary ---------------------------------------------
     const int mode = reached < m ? 0 : 1;
-    const int count = mode == 0 ? m : nL;
+    if (mode == 1) {   // the sequence is the deepest check level
+        L.seg = ld_cg(A.lvl_seg);
+        L.total = load_prefix(A.lvl_cnt, s_pre, sh);
+    }
+    const int count = mode == 0 ? m : L.total;
     auto cand_deg = [&](long long i) -> int {   // degree at sequence position i, INF if not a candidate
         if (mode == 0) return ld_cg(A.vis_c + i) == token ? INF : ld_cg(A.cn_deg + i);
-        return ld_cg(A.cn_deg + ld_cg(A.lvl + i));
+        return ld_cg(A.cn_deg + L.at(i));
     };
     const long long seg = ((long long)count + gridDim.x - 1) / gridDim.x;
     const long long s0 = min((long long)count, (long long)blockIdx.x * seg), s1 = min((long long)count, s0 + seg);
@@ -408,11 +429,15 @@ __global__ void __launch_bounds__(PB) peg_step_kernel(PegArgs A, int v, int toke
         s_first[d] = INF;
     }
     __syncthreads();
-    for (long long i = s0 + threadIdx.x; i < s1; i += PB) {
-        const int d = cand_deg(i);
-        if (d < ND) {
-            atomicAdd(&s_cnt[d], 1);
-            atomicMin(&s_first[d], (int)i);
+    for (long long c0 = s0; c0 < s1; c0 += PB) {
+        if (mode == 1) L.tile(c0);
+        const long long i = c0 + threadIdx.x;
+        if (i < s1) {
+            const int d = cand_deg(i);
+            if (d < ND) {
+                atomicAdd(&s_cnt[d], 1);
+                atomicMin(&s_first[d], (int)i);
+            }
         }
     }
     __syncthreads();
@@ -437,7 +462,7 @@ __global__ void __launch_bounds__(PB) peg_step_kernel(PegArgs A, int v, int toke
         __syncthreads();
     }
     if (dmin >= INF) {   // no candidate at all
-        if (gtid == 0) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
             A.sum->mode = mode; A.sum->count = count; A.sum->dmin = INF; A.sum->p0 = INF; A.sum->kstar = 0;
         }
         return;
@@ -456,6 +481,7 @@ __global__ void __launch_bounds__(PB) peg_step_kernel(PegArgs A, int v, int toke
     // running-minimum ties before p0 (draws whose outcome p0 overwrites)
     int tb = 0;
     for (long long c0 = s0; c0 < s1 && c0 < p0; c0 += PB) {
+        if (mode == 1) L.tile(c0);
         const long long i = c0 + threadIdx.x;
         const int dd = (i < s1 && i < p0) ? cand_deg(i) : INF;
         int tmin;
@@ -464,7 +490,7 @@ __global__ void __launch_bounds__(PB) peg_step_kernel(PegArgs A, int v, int toke
         rin = min(rin, tmin);
     }
     if (threadIdx.x == 0 && tb) atomicAdd(&A.sum->t_pre, (unsigned long long)tb);
-    if (gtid == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
         A.sum->mode = mode;
         A.sum->count = count;
         A.sum->dmin = dmin;
@@ -572,9 +598,15 @@ int mbp_peg_build_device(int32_t n, int32_t m, const int32_t* col_deg, uint64_t 
     PEG_CUDA(mem.alloc(&A.vis_v, n, 0));
     PEG_CUDA(mem.alloc(&A.key_c, m, 0xff));
     PEG_CUDA(mem.alloc(&A.key_v, n, 0xff));
-    PEG_CUDA(mem.alloc(&A.lvl, m, 0));
-    PEG_CUDA(mem.alloc(&A.fr, n, 0));
-    PEG_CUDA(mem.alloc(&A.blk, grid, 0));
+    // regions: a level's slots can outnumber its nodes, and each block owns
+    // a segment of ceil(slots / grid) entries
+    const size_t reg_c = (size_t)n * KV + grid, reg_v = (size_t)m * KC + grid;
+    PEG_CUDA(mem.alloc(&A.lvl, reg_c, 0));
+    PEG_CUDA(mem.alloc(&A.fr, std::max(reg_v, (size_t)n), 0));
+    PEG_CUDA(mem.alloc(&A.lvl_cnt, grid, 0));
+    PEG_CUDA(mem.alloc(&A.fr_cnt, grid, 0));
+    PEG_CUDA(mem.alloc(&A.lvl_seg, 1, 0));
+    PEG_CUDA(mem.alloc(&A.fr_seg, 1, 0));
     PEG_CUDA(mem.alloc(&A.blk_k, grid, 0));
     PEG_CUDA(mem.alloc(&A.blk_min, grid, 0));
     PEG_CUDA(mem.alloc(&A.st_cnt, (size_t)grid * ND, 0));
@@ -600,11 +632,17 @@ int mbp_peg_build_device(int32_t n, int32_t m, const int32_t* col_deg, uint64_t 
     int token = 0;
     int attach_v = -1;
     unsigned long long attach_j = 0;
+    int kc = 1;   // effective check-adjacency slots: the largest check degree so far
     auto launch = [&](int v, int tok, int do_bfs) -> cudaError_t {
-        void* args[] = {(void*)&A, (void*)&v, (void*)&tok, (void*)&attach_v, (void*)&attach_j, (void*)&do_bfs};
+        void* args[] = {(void*)&A, (void*)&v, (void*)&tok, (void*)&attach_v, (void*)&attach_j, (void*)&do_bfs,
+                        (void*)&kc};
         return cudaLaunchCooperativeKernel((const void*)peg_step_kernel, dim3(grid), dim3(PB), args, 0, s);
     };
     for (int v = 0; v < n; ++v) {
+        if (debug >= 2 && v && (v & 0xffff) == 0)
+            fprintf(stderr, "peg_gpu seed=%llu: %d/%d variables, %.0f s, %.1f s GPU, %.1f s stream\n",
+                    (unsigned long long)seed, v, n, std::chrono::duration<double>(now() - t_start).count(), t_wait,
+                    t_rng);
         for (int e = 0; e < col_deg[v]; ++e) {
             ++token;
             const auto t0 = now();
@@ -631,6 +669,7 @@ int mbp_peg_build_device(int32_t n, int32_t m, const int32_t* col_deg, uint64_t 
                         v, e, hs->mode, hs->count, hs->dmin, hs->p0, hs->t_pre, hs->kstar, win, hs->winner);
             attach_v = v;
             attach_j = win;
+            kc = std::min(KC, std::max(kc, hs->dmin + 1));   // the winner's new degree
         }
     }
     if (debug >= 2)
