@@ -52,3 +52,25 @@ def test_measure_throughput_modes_match_reference(cfg1_ensemble, name, kw):
     for k in ("mean_iterations", "success_rate", "residual_error_rate", "frames"):
         assert getattr(p, k) == g[k], k
     assert abs(p.iterations_std - g["iterations_std"]) < 1e-12
+
+
+@pytest.mark.gpu
+def test_cli_backend_hook_runs_the_reference_sweep(cfg1_ensemble):
+    """The names cli_backend.install puts into mmrecon.cli give the
+    reference's rows (the same golden as run_sweep above)."""
+    import types
+
+    from paper_2001_07979_b200 import cli_backend
+
+    mod = types.SimpleNamespace(measure_throughput=None, run_sweep=None)
+    cli_backend.install(mod)
+    spec = SweepSpec(e_values=(0.03, 0.09, 0.2), u_values=(1, 2), ensembles={0.5: cfg1_ensemble}, frames=24,
+                     warmup=2, seed=3)
+    rows = mod.run_sweep(spec, io.StringIO())
+    for r, g in zip(rows, GOLD["rows"]):
+        for k in KEEP:
+            assert getattr(r, k) == g[k], (k, r, g)
+    p = mod.measure_throughput(cfg1_ensemble, 2, 0.07, 20, seed=4, warmup=1, point_path=(5,), prior_e=0.05)
+    g = GOLD["points"]["prior"]
+    for k in ("mean_iterations", "success_rate", "residual_error_rate", "frames"):
+        assert getattr(p, k) == g[k], k
