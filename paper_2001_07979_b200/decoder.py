@@ -417,8 +417,13 @@ class DecoderWorkspace:
     """Per-frame message buffers for one ensemble (decoder.py:80-134).
 
     Host float64 arrays with the reference's stacked layout; after ``decode``
-    they mirror the device state (posterior, c2v, v2c, hard).  The device
-    buffers live in a ``BatchDecoder`` of capacity one frame."""
+    they hold the final state as the reference's would (posterior, c2v, v2c,
+    hard).  ``decode`` runs the production (scatter) kernel, which keeps no
+    messages; the message arrays are materialised on first access by
+    replaying the frame on the explicit-message kernel (same decisions, same
+    iteration count -- tests/test_gpu_scatter.py), so callers that never read
+    them (bench.measure_throughput, session._decode_block) do not pay for
+    it."""
 
     def __init__(self, ensemble, config=None):
         self.ensemble = ensemble
@@ -432,20 +437,39 @@ class DecoderWorkspace:
         self.var_edge = lay.var_edge
         total = lay.edges
         n = lay.n
-        self.v2c = np.zeros(total, dtype=np.float64)
-        self.c2v = np.zeros(total, dtype=np.float64)
+        self._v2c = np.zeros(total, dtype=np.float64)
+        self._c2v = np.zeros(total, dtype=np.float64)
         self.priors = np.zeros(n, dtype=np.float64)
-        self.posterior = np.zeros(n, dtype=np.float64)
+        self._posterior = np.zeros(n, dtype=np.float64)
         self.hard = np.zeros(n, dtype=np.uint8)
         self.iteration = 0
         self._dec = None
         self._dec_key = None
+        self._fast = None
+        self._fast_key = None
+        self._pending = None     # (noisy row, syndrome row, e, config) of a decode not yet mirrored
+
+    # message state, materialised on demand
+    def _state(self, name):
+        if self._pending is not None:
+            _materialize(self)
+        return getattr(self, name)
+
+    def _set_state(self, name, value):
+        if self._pending is not None:
+            _materialize(self)
+        getattr(self, name)[...] = value
+
+    v2c = property(lambda self: self._state("_v2c"), lambda self, v: self._set_state("_v2c", v))
+    c2v = property(lambda self: self._state("_c2v"), lambda self, v: self._set_state("_c2v", v))
+    posterior = property(lambda self: self._state("_posterior"), lambda self, v: self._set_state("_posterior", v))
 
     def reset(self) -> None:
-        self.v2c[:] = 0.0
-        self.c2v[:] = 0.0
+        self._pending = None
+        self._v2c[:] = 0.0
+        self._c2v[:] = 0.0
         self.priors[:] = 0.0
-        self.posterior[:] = 0.0
+        self._posterior[:] = 0.0
         self.hard[:] = 0
         self.iteration = 0
 
@@ -453,7 +477,7 @@ class DecoderWorkspace:
         return slice(int(self.edge_off[l]), int(self.edge_off[l + 1]))
 
     def _device(self, config: DecoderConfig, track: bool) -> BatchDecoder:
-        # the fine-grained API reads messages back: explicit-message kernel
+        # state readback: the explicit-message kernel with kept state
         flags = N.MBP_KEEP_STATE | N.MBP_EXPLICIT_MESSAGES | (N.MBP_RECORD_HISTORY if track else 0)
         shape_key = (config.precision, config.combining_mode)
         if self._dec is None or self._dec_key != shape_key:
@@ -462,6 +486,35 @@ class DecoderWorkspace:
         elif self._dec.config != config or self._dec.flags != flags:
             self._dec.configure(config, flags)
         return self._dec
+
+    def _production(self, config: DecoderConfig, track: bool) -> BatchDecoder:
+        # decisions only: the production path, no kept state
+        flags = N.MBP_RECORD_HISTORY if track else 0
+        shape_key = (config.precision, config.combining_mode)
+        if self._fast is None or self._fast_key != shape_key:
+            self._fast = BatchDecoder(self.ensemble, 1, config, flags=flags)
+            self._fast_key = shape_key
+        elif self._fast.config != config or self._fast.flags != flags:
+            self._fast.configure(config, flags)
+        return self._fast
+
+
+def _materialize(ws: DecoderWorkspace) -> None:
+    """Mirror the final device state of the last decode into the workspace
+    arrays: replay the frame on the explicit-message kernel with kept state."""
+    noisy, syn, e, config, iters = ws._pending
+    ws._pending = None
+    lay = ws.layout
+    if iters == 0:
+        ws._v2c[:] = ws.priors[lay.chk_var]
+        ws._c2v[:] = 0.0
+        ws._posterior[:] = 0.0
+        return
+    dec = ws._device(config, False)
+    dec.decode(noisy, syn, e)
+    ws._c2v[:] = dec.c2v(0)
+    ws._posterior[:] = dec.posterior(0)
+    ws._v2c[:] = _final_v2c(ws, config, dec)
 
 
 def _matrices(ensemble_or_matrix):
@@ -566,30 +619,35 @@ def decode(ensemble, noisy_key, syndromes, e: float, config=None, workspace=None
     for l, z in enumerate(syndromes):
         if z.length != m:
             raise ValueError(f"syndrome {l} length {z.length} != m={m}")
+    if not 0.0 < e < 0.5:
+        raise ValueError(f"crossover probability must be in (0, 0.5), got {e}")
+    noisy = np.asarray(noisy_key.data, dtype=np.uint8).reshape(1, -1)
+    syn = np.concatenate([np.asarray(z.data, dtype=np.uint8) for z in syndromes]).reshape(1, -1)
     if workspace is None:
-        workspace = DecoderWorkspace(ensemble, config)
-    elif not _same_ensemble(workspace.ensemble, ensemble):
+        # nothing to mirror: a per-thread production decoder, no state kept
+        dec = _thread_decoder(ensemble, config, track_decisions)
+        res = dec.decode(noisy, syn, e)
+        iters = int(res.iterations[0])
+        return DecodeResult(
+            corrected=BitBlock(res.corrected[0].copy(), n),
+            converged=bool(res.converged[0]),
+            iterations_used=iters,
+            residual_syndrome_mismatches=int(res.mismatches[0]),
+            decision_history=dec.history(0, iters + 1) if track_decisions else None,
+        )
+    if not _same_ensemble(workspace.ensemble, ensemble):
         raise ValueError("workspace was built for a different ensemble")
     workspace.config = config
     workspace.reset()
     workspace.priors[:] = init_priors(noisy_key, e)
 
-    dec = workspace._device(config, track_decisions)
-    noisy = np.asarray(noisy_key.data, dtype=np.uint8).reshape(1, -1)
-    syn = np.concatenate([np.asarray(z.data, dtype=np.uint8) for z in syndromes]).reshape(1, -1)
+    dec = workspace._production(config, track_decisions)
     res = dec.decode(noisy, syn, e)
     iters = int(res.iterations[0])
-
-    # mirror the device state into the reference-layout host arrays
-    lay = workspace.layout
     workspace.hard[:] = np.unpackbits(res.corrected[0], count=n, bitorder="little")
-    if iters == 0:
-        workspace.v2c[:] = workspace.priors[lay.chk_var]
-    else:
-        workspace.c2v[:] = dec.c2v(0)
-        workspace.posterior[:] = dec.posterior(0)
-        workspace.v2c[:] = _final_v2c(workspace, config, dec)
     workspace.iteration = iters
+    # the message arrays follow on first access (DecoderWorkspace._state)
+    workspace._pending = (noisy.copy(), syn.copy(), float(e), config, iters)
     history = dec.history(0, iters + 1) if track_decisions else None
     return DecodeResult(
         corrected=BitBlock(res.corrected[0].copy(), n),
@@ -598,6 +656,30 @@ def decode(ensemble, noisy_key, syndromes, e: float, config=None, workspace=None
         residual_syndrome_mismatches=int(res.mismatches[0]),
         decision_history=history,
     )
+
+
+_TLS = threading.local()
+
+
+def _thread_decoder(ensemble, config: DecoderConfig, track: bool) -> BatchDecoder:
+    """A one-frame production decoder per (thread, matrix set, precision,
+    combining mode): decode() without a workspace is called from worker
+    threads (the reference's measure_throughput, session._decode_block), and
+    a device workspace must not be shared between threads."""
+    cache = getattr(_TLS, "decoders", None)
+    if cache is None:
+        cache = _TLS.decoders = OrderedDict()
+    key = (_content_key(ensemble), config.precision, config.combining_mode)
+    dec = cache.get(key)
+    flags = N.MBP_RECORD_HISTORY if track else 0
+    if dec is None:
+        dec = BatchDecoder(ensemble, 1, config, flags=flags)
+        cache[key] = dec
+        while len(cache) > 4:
+            cache.popitem(last=False)
+    elif dec.config != config or dec.flags != flags:
+        dec.configure(config, flags)
+    return dec
 
 
 def _final_v2c(ws: DecoderWorkspace, cfg: DecoderConfig, dec: BatchDecoder) -> np.ndarray:

@@ -314,8 +314,24 @@ def _matrices_of(ensemble_or_matrix):
     return (ensemble_or_matrix,)
 
 
+_LAYOUTS: dict = {}
+
+
 def stacked_layout(ensemble) -> StackedLayout:
+    """The stacked layout of an ensemble (immutable; memoised by the
+    matrices' content hashes, so a layout is built once per matrix set)."""
     mats = _matrices_of(ensemble)
+    key = tuple(h.content_hash() for h in mats)
+    lay = _LAYOUTS.get(key)
+    if lay is None:
+        lay = _build_stacked_layout(mats)
+        if len(_LAYOUTS) >= 8:
+            _LAYOUTS.pop(next(iter(_LAYOUTS)))
+        _LAYOUTS[key] = lay
+    return lay
+
+
+def _build_stacked_layout(mats) -> StackedLayout:
     n, m, u = mats[0].n, mats[0].m, len(mats)
     counts = [int(np.asarray(h.chk_var).shape[0]) for h in mats]
     edge_off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)

@@ -121,3 +121,42 @@ def test_two_ranks_shard_the_stream_on_the_gpu():
     ok, work = q.get()
     assert ok
     assert work == [32.0]
+
+
+def test_dropin_decode_per_frame_threads_and_lazy_state(cfg1_ensemble):
+    """The reference's measure_throughput pattern: decode() per frame from
+    worker threads, with and without a per-thread workspace.  Results equal
+    the batched path; a workspace's messages appear on first access and
+    equal the eager explicit-kernel readback."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2001_07979_b200 import BitBlock, DecoderWorkspace, decode
+    from paper_2001_07979_b200.decoder import _final_v2c
+
+    ens = cfg1_ensemble
+    fb = make_frames(ens.n, 0.07, 24, seed=9)
+    dec = BatchDecoder(ens, 24)
+    syn = dec.syndromes(fb.keys)
+    ref = dec.decode(fb.noisy, syn, 0.07)
+    mb = (ens.m + 7) // 8
+
+    def one(k, ws=None):
+        return decode(ens, BitBlock(fb.noisy[k], ens.n),
+                      [BitBlock(syn[k, l * mb:(l + 1) * mb], ens.m) for l in range(ens.u)], 0.07, workspace=ws)
+
+    with ThreadPoolExecutor(4) as pool:
+        got = list(pool.map(one, range(24)))
+    for k, r in enumerate(got):
+        assert r.converged == bool(ref.converged[k]) and r.iterations_used == int(ref.iterations[k])
+        assert np.array_equal(r.corrected.data, ref.corrected[k])
+    ws = DecoderWorkspace(ens)
+    for k in (0, 5, 11):
+        r = one(k, ws)
+        assert r.iterations_used == int(ref.iterations[k])
+        assert ws._pending is not None                      # nothing read back yet
+        c2v, post, v2c = ws.c2v.copy(), ws.posterior.copy(), ws.v2c.copy()
+        assert ws._pending is None
+        eager = ws._device(ws.config, False)
+        eager.decode(fb.noisy[k:k + 1], syn[k:k + 1], 0.07)
+        assert np.array_equal(c2v, eager.c2v(0)) and np.array_equal(post, eager.posterior(0))
+        assert np.array_equal(v2c, _final_v2c(ws, ws.config, eager))
