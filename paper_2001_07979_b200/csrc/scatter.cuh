@@ -71,7 +71,9 @@ constexpr int kVB = 96;         // 32-bit words per variable block (3 lines)
 #define MBP_SCATTER_MIN_BLOCKS 4
 #endif
 // resident blocks per SM: 64 registers up to degree 8; wider rows keep two
-// rows' gathers in flight and need 128 (no spills)
+// rows' gathers in flight and get 128.  Both budgets spill (ptxas -v: D = 7
+// 3.4 KB, D = 14 2.0 KB of spill stores, mostly cold paths: the explicit-base
+// and saturation variants); measured trade-off in DESIGN.md §10
 template <int D>
 constexpr int scatter_min_blocks() { return D <= 8 ? MBP_SCATTER_MIN_BLOCKS : 2; }
 
@@ -548,32 +550,42 @@ __device__ __forceinline__ void sc_var1_chunk(const ScatterArgs& A, const SL<CPT
             const int Lf = S.Lfix(g * 32 + lane);
             const unsigned lbit = 1u << lane;
             if (act == kFull && !A.hist_w) {
-                // every lane live, no history: two variables per pass, no predicates
+                // every lane live, no history: UV variables per pass, no predicates
+#ifndef MBP_V1_UV
+#define MBP_V1_UV 2
+#endif
+                constexpr int UV = MBP_V1_UV;
                 int v = r;
-                for (; v + 1 < r + span; v += 2) {
-                    int a0 = Lf, a1 = Lf;
+                for (; v + UV - 1 < r + span; v += UV) {
+                    int a[UV];
+#pragma unroll
+                    for (int q = 0; q < UV; ++q) a[q] = Lf;
 #pragma unroll
                     for (int k = 0; k < DV; ++k) {
-                        const int m0 = s_mf[s_deg[v * DV + k] * 32 + lane];
-                        const int m1 = s_mf[s_deg[(v + 1) * DV + k] * 32 + lane];
-                        a0 += (s_mis[v * DV + k] & lbit) ? -m0 : m0;
-                        a1 += (s_mis[(v + 1) * DV + k] & lbit) ? -m1 : m1;
+#pragma unroll
+                        for (int q = 0; q < UV; ++q) {
+                            const int mq = s_mf[s_deg[(v + q) * DV + k] * 32 + lane];
+                            a[q] += (s_mis[(v + q) * DV + k] & lbit) ? -mq : mq;
+                        }
                     }
                     const size_t w = (size_t)base + v;
                     float* vr = S.vrow(w, lane);
-                    vr[32] = (float)a0 * iscale;
-                    reinterpret_cast<int*>(vr)[64] = a0;   // acc = post'_1 in fixed point
-                    vr[kVB + 32] = (float)a1 * iscale;
-                    reinterpret_cast<int*>(vr)[kVB + 64] = a1;
-                    const unsigned y0 = s_y[v] & lbit, y1 = s_y[v + 1] & lbit;
-                    const unsigned n0 = __ballot_sync(kFull, y0 ? a0 > 0 : a0 < 0);
-                    const unsigned n1 = __ballot_sync(kFull, y1 ? a1 > 0 : a1 < 0);
-                    if (lane == 0) {
-                        S.hard_w()[w] = n0;
-                        S.hard_w()[w + 1] = n1;
+                    unsigned nq[UV];
+#pragma unroll
+                    for (int q = 0; q < UV; ++q) {
+                        vr[q * kVB + 32] = (float)a[q] * iscale;
+                        reinterpret_cast<int*>(vr)[q * kVB + 64] = a[q];   // acc = post'_1 in fixed point
+                        const unsigned yq = s_y[v + q] & lbit;
+                        nq[q] = __ballot_sync(kFull, yq ? a[q] > 0 : a[q] < 0);
+                    }
+                    if (lane < UV) {
+                        unsigned hw = nq[0];
+#pragma unroll
+                        for (int q = 1; q < UV; ++q) hw = lane == q ? nq[q] : hw;
+                        S.hard_w()[w + lane] = hw;
                     }
                 }
-                if (v < r + span) {
+                for (; v < r + span; ++v) {
                     int a0 = Lf;
 #pragma unroll
                     for (int k = 0; k < DV; ++k) {
