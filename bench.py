@@ -65,8 +65,11 @@ WORKLOADS = {
     "cfg1": ("cfg1_n4096_m2048_u2_s1.npz", "u=2 PEG n=4096 m=2048 R=0.5 (reference build_ensemble seeds 1,2)"),
     "cfg2": ("cfg2_n65536_m32768_u2_s1.npz", "u=2 PEG n=65536 m=32768 R=0.5 (reference build_ensemble seeds 1,2)"),
     "cfg3": ("cfg3_n65536_m14650_u3_s11.npz", "u=3 PEG n=65536 m=14650 (f=1.15 at e=0.03; reference seeds 11-13)"),
-    "cfg4": (None, "u=2 n=1048576 m=524288 R=0.5 SYNTHETIC random (3,6)-regular graphs (seeds 7,8)"),
+    "cfg4": ("cfg4_n1048576_m524288_u2_s1.npz",
+             "u=2 PEG n=1048576 m=524288 R=0.5 (build_ensemble base_seed=1 on the device PEG: the reference's "
+             "matrices)"),
 }
+CFG4_SYNTHETIC = "u=2 n=1048576 m=524288 R=0.5 SYNTHETIC random (3,6)-regular graphs (seeds 7,8)"
 L2_FLUSH_BYTES = 256 << 20   # > 126 MB L2: written between timed steps
 KERNELS_PER_DECODE = 5       # setup, 2 row->word transposes, decode, word->row transpose
 
@@ -242,12 +245,25 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples), "source": self.source}
 
 
+def ensemble_path(workload):
+    return ROOT / "paper_2001_07979_b200" / "ensembles" / WORKLOADS[workload][0]
+
+
+def workload_text(workload):
+    if workload == "cfg4" and not ensemble_path(workload).exists():
+        return CFG4_SYNTHETIC
+    return WORKLOADS[workload][1]
+
+
 def load_ensemble_for(workload):
+    """The workload's PEG ensemble; cfg 4 falls back to synthetic random
+    regular graphs when its 2^20 PEG cache is not present."""
     from paper_2001_07979_b200.matrix import load_ensemble, random_regular_ensemble
 
-    fname = WORKLOADS[workload][0]
-    return (load_ensemble(ROOT / "paper_2001_07979_b200" / "ensembles" / fname) if fname
-            else random_regular_ensemble(1 << 20, 1 << 19, 2, seed=7))
+    p = ensemble_path(workload)
+    if workload == "cfg4" and not p.exists():
+        return random_regular_ensemble(1 << 20, 1 << 19, 2, seed=7)
+    return load_ensemble(p)
 
 
 def device_frames(dec, n, e, lo, count, device):
@@ -419,7 +435,7 @@ def config_dict(args, ens, world, devices):
     par = f"dp{world} (contiguous frame shards, no collective on the data path)"
     if devices < world:
         par += f"; {world} ranks on {devices} GPU(s), round-robin"
-    return {"workload": f"{args.workload}: {WORKLOADS[args.workload][1]}, "
+    return {"workload": f"{args.workload}: {workload_text(args.workload)}, "
                         f"BSC e={args.e}, {args.frames}-frame batch per GPU",
             "n": ens.n, "m": ens.m, "u": ens.u, "e": args.e, "f": round(efficiency(ens.m, ens.n, args.e), 4),
             "frames_per_gpu": args.frames, "max_iterations": 60, "llr_clamp": 30.0,
@@ -462,7 +478,7 @@ def side_config(workload, e, precision, frames, steps, device, flush, stream):
     ev_ms, wall_ms = host_call(dec, noisy_h.a, syn_h.a, e, res)
     g2 = int((res.converged.astype(bool) & np.all(res.corrected == keys_h, axis=1)).sum()) * n
     return {
-        "workload": WORKLOADS[workload][1], "e": e, "precision": precision, "frames": frames,
+        "workload": workload_text(workload), "e": e, "precision": precision, "frames": frames,
         "value": round(value, 3), "unit": "Mbps", "ms_per_step": round(statistics.mean(step_ms), 4),
         "kernel_ms": round(statistics.mean(kms), 4),
         "e2e": {"value": round(g2 / (ev_ms / 1e3) / 1e6, 3), "host_wall_value": round(g2 / (wall_ms / 1e3) / 1e6, 3),
@@ -729,7 +745,8 @@ def main():
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32" if args.precision == "fp32" else "f64",
         "data": "synthetic (the reference's Philox frame streams, generated on the GPU bit for bit; "
-                + ("synthetic random regular graphs)" if args.workload == "cfg4" else "PEG ensemble from the reference)"),
+                + ("synthetic random regular graphs)" if workload_text(args.workload) == CFG4_SYNTHETIC
+                   else "PEG ensemble of the reference)"),
         "config": config_dict(args, ens, world, devices),
         "timing": ("host clock over the barrier-synchronised job span (ranks time-slice shared GPUs)" if _SHARED
                    else "CUDA events on each rank's launching stream, max over ranks"),

@@ -162,11 +162,14 @@ def test_host_path_pipelining_is_transparent(cfg2_ensemble, subbatches):
 @pytest.fixture(scope="module")
 def cfg4_ensemble():
     """u = 2, n = 2^20, m = 2^19 (BASELINE configs[3], long-key frames whose
-    messages far exceed shared memory and L2).  SYNTHETIC random (3, 6)-regular
-    graphs: the reference's PEG needs ~7 h per matrix at this size."""
-    from paper_2001_07979_b200.matrix import random_regular_ensemble
+    messages far exceed shared memory and L2): the PEG cache built by the
+    device PEG (build_ensemble(2^20, 2^19, 3, u=2, base_seed=1)) when it is
+    committed, else synthetic random (3, 6)-regular graphs."""
+    from conftest import ENSEMBLES
+    from paper_2001_07979_b200.matrix import load_ensemble, random_regular_ensemble
 
-    return random_regular_ensemble(1 << 20, 1 << 19, 2, seed=7)
+    p = ENSEMBLES / "cfg4_n1048576_m524288_u2_s1.npz"
+    return load_ensemble(p) if p.exists() else random_regular_ensemble(1 << 20, 1 << 19, 2, seed=7)
 
 
 def test_long_key_cfg4_against_oracle(cfg4_ensemble):
