@@ -50,6 +50,7 @@ constexpr int PB = 512;        // threads per block
 constexpr int INF = 1 << 30;
 constexpr int ND = KC + 1;     // candidate degrees 0..KC
 constexpr long long kSmallLevel = 8192;   // slots block 0 expands alone
+constexpr int kMaxHalfLevels = (1 << 18) - 2;   // BFS depth bound of the key format
 
 struct PegSummary {
     int mode;                  // 0: unreached checks in index order, 1: deepest level in BFS order
@@ -93,8 +94,10 @@ struct PegArgs {
 // the expansion that wrote it (slot numbers restart every half-level).
 __device__ __forceinline__ unsigned long long mk(int token, int hl, long long slot)
 {
-    const unsigned hi = ~((unsigned)token * 1024u + (unsigned)hl);   // token < 2^22, hl < 1024
-    return ((unsigned long long)hi << 32) | (unsigned long long)slot;
+    // [40 bits: ~(token << 18 | hl)] [24 bits: slot]; token < 2^22, hl < 2^18,
+    // slot < 2^24 (an expansion has at most max(4n, 16m) slots)
+    const unsigned long long hi = ~(((unsigned long long)token << 18) | (unsigned long long)hl) & ((1ull << 40) - 1);
+    return (hi << 24) | (unsigned long long)slot;
 }
 
 // block-wide exclusive sum of one int per thread; returns the block total in *tot
@@ -369,7 +372,7 @@ __global__ void __launch_bounds__(PB) peg_step_kernel(PegArgs A, int v, int toke
                     if (nF == 0) { done = 1; break; }
                     stage = 0;
                 }
-                if (hl >= 1022) { done = 1; if (threadIdx.x == 0) A.sum->overflow = 1; break; }
+                if (hl >= kMaxHalfLevels) { done = 1; if (threadIdx.x == 0) A.sum->overflow = 1; break; }
             }
             if (threadIdx.x == 0) {
                 A.bfs[0] = nF; A.bfs[1] = nL; A.bfs[2] = reached; A.bfs[3] = hl; A.bfs[4] = stage; A.bfs[5] = done;
@@ -403,7 +406,7 @@ __global__ void __launch_bounds__(PB) peg_step_kernel(PegArgs A, int v, int toke
             if (nF == 0) break;
             stage = 0;
         }
-        if (hl >= 1022) {
+        if (hl >= kMaxHalfLevels) {
             if (blockIdx.x == 0 && threadIdx.x == 0) A.sum->overflow = 1;
             break;
         }
@@ -575,6 +578,8 @@ int mbp_peg_build_device(int32_t n, int32_t m, const int32_t* col_deg, uint64_t 
         E += col_deg[i];
     }
     if (E >= (1 << 22)) return mbp::set_error(MBP_EUNSUPPORTED, "device PEG supports < 2^22 edges");
+    if ((long long)n * KV >= (1 << 24) || (long long)m * KC >= (1 << 24))
+        return mbp::set_error(MBP_EUNSUPPORTED, "device PEG supports n < 2^22 and m < 2^20");
     int prev_dev = 0;
     cudaGetDevice(&prev_dev);
     PEG_CUDA(cudaSetDevice(device));
@@ -652,7 +657,7 @@ int mbp_peg_build_device(int32_t n, int32_t m, const int32_t* col_deg, uint64_t 
             const auto t1 = now();
             t_wait += std::chrono::duration<double>(t1 - t0).count();
             if (hs->overflow)
-                return mbp::set_error(MBP_EUNSUPPORTED, "device PEG capacity exceeded (check degree > 16 or BFS depth > 1000)");
+                return mbp::set_error(MBP_EUNSUPPORTED, "device PEG capacity exceeded (check degree > 16 or BFS depth > 2^18)");
             if (hs->dmin >= INF) return mbp::set_error(MBP_EUNSUPPORTED, "PEG found no attachable check node");
             // the tie-break stream: T_pre draws whose outcome p0 overwrites,
             // then one draw per degree-dmin candidate after p0 (ties 2, 3, ...)

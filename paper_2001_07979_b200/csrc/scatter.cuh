@@ -162,7 +162,7 @@ struct SL {
 // integer, ties to even, when |c * 2^S| < 2^22 -- the kernel caps S for
 // that) instead of F2I, which issues on the XU pipe next to the rule's MUFUs.
 #ifndef MBP_FIX_MAGIC
-#define MBP_FIX_MAGIC 0
+#define MBP_FIX_MAGIC 1
 #endif
 __device__ __forceinline__ int fixq(float c, float scale)
 {
@@ -211,26 +211,39 @@ __device__ __forceinline__ void rule_sd(const float (&x)[DD], int d, unsigned fl
         sb[k] = in ? (__float_as_uint(x[k]) & 0x80000000u) : 0u;
         tot ^= sb[k];
     }
+    // The first factor of each pass is (1, 0) x (1, u) = (1, u) exactly (u is
+    // finite, in [0, 1]): written out so that the compiler folds the
+    // multiplications by 1 and 0 it cannot prove away (0 * u for a NaN u).
     float sS[DD], sD[DD];
     float S = 1.0f, Dl = 0.0f;
 #pragma unroll
     for (int k = DD - 1; k >= 0; --k) {
         sS[k] = S;
         sD[k] = Dl;
-        const float S2 = fmaf(Dl, uu[k], S);
-        Dl = fmaf(S, uu[k], Dl);
-        S = S2;
+        if (k == DD - 1) {
+            S = 1.0f;
+            Dl = uu[k];
+        } else {
+            const float S2 = fmaf(Dl, uu[k], S);
+            Dl = fmaf(S, uu[k], Dl);
+            S = S2;
+        }
     }
     float pS = 1.0f, pD = 0.0f;
 #pragma unroll
     for (int k = 0; k < DD; ++k) {
-        const float eS = fmaf(pS, sS[k], pD * sD[k]);
-        const float eD = fmaf(pS, sD[k], pD * sS[k]);
+        const float eS = k == 0 ? sS[k] : fmaf(pS, sS[k], pD * sD[k]);
+        const float eD = k == 0 ? sD[k] : fmaf(pS, sD[k], pD * sS[k]);
         const float mag = fminf(lg2_approx(eS) - lg2_approx(eD), clamp);
         out[k] = __uint_as_float(__float_as_uint(mag) | (tot ^ sb[k]));
-        const float S2 = fmaf(pD, uu[k], pS);
-        pD = fmaf(pS, uu[k], pD);
-        pS = S2;
+        if (k == 0) {
+            pS = 1.0f;
+            pD = uu[k];
+        } else {
+            const float S2 = fmaf(pD, uu[k], pS);
+            pD = fmaf(pS, uu[k], pD);
+            pS = S2;
+        }
     }
 }
 
