@@ -187,6 +187,15 @@ int mbp_peg_build(int32_t n, int32_t m, const int32_t *col_deg, uint64_t seed, i
  * instead of hours.  Column degrees <= 4, check degrees <= 16.           */
 int mbp_peg_build_device(int32_t n, int32_t m, const int32_t *col_deg, uint64_t seed,
                          int64_t *chk_ptr, int32_t *chk_var, int device);
+/* The same construction in stages: variables [v_begin, v_end) on top of the
+ * graph in vn_adj ([n][4] int32 check ids per variable in edge order, -1 =
+ * none; rows < v_begin complete), which receives the new rows; *state is the
+ * tie-break stream at v_begin (derived from seed when v_begin == 0) and at
+ * v_end on return.  Stages chained over [0, n) give mbp_peg_build_device's
+ * matrix (a long build can checkpoint and resume).                        */
+int mbp_peg_build_device_range(int32_t n, int32_t m, const int32_t *col_deg, uint64_t seed,
+                               uint64_t *state, int32_t v_begin, int32_t v_end, int32_t *vn_adj,
+                               int device);
 
 /* ---- synthetic BSC frames (the reference's frame streams) ---------------
  * Rows [batch][ceil(n/8)] of Alice's keys and Bob's noisy keys for frames

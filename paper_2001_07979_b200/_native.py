@@ -30,7 +30,8 @@ EXPORTS = (
     "mbp_workspace_read_history", "mbp_workspace_read_phase_times",
     "mbp_c2v_pass", "mbp_v2c_pass", "mbp_posterior_pass",
     "mbp_host_alloc", "mbp_host_free", "mbp_workspace_last_timing", "mbp_workspace_last_stats",
-    "mbp_peg_build", "mbp_peg_build_device", "mbp_frames_generate_device", "mbp_frames_generate",
+    "mbp_peg_build", "mbp_peg_build_device", "mbp_peg_build_device_range",
+    "mbp_frames_generate_device", "mbp_frames_generate",
 )
 
 
@@ -80,6 +81,8 @@ _SIGS = {
     "mbp_host_alloc": ([C.c_size_t], _VP),
     "mbp_peg_build": ([C.c_int32, C.c_int32, _VP, C.c_uint64, _VP, _VP], C.c_int),
     "mbp_peg_build_device": ([C.c_int32, C.c_int32, _VP, C.c_uint64, _VP, _VP, C.c_int], C.c_int),
+    "mbp_peg_build_device_range": ([C.c_int32, C.c_int32, _VP, C.c_uint64, C.POINTER(C.c_uint64), C.c_int32,
+                                    C.c_int32, _VP, C.c_int], C.c_int),
     "mbp_host_free": ([_VP], None),
     "mbp_frames_generate_device": ([C.c_int32, _VP, C.c_int32, C.c_int64, C.c_int64, C.c_double, _VP, _VP, _VP],
                                    C.c_int),

@@ -269,6 +269,39 @@ __device__ __forceinline__ void expand(const PegArgs& A, int token, int hl, cons
     if (grid_mode) grid_barrier(A.bar); else __syncthreads();
 }
 
+// A level of at most 32 slots on warp 0 alone (the long, thin BFSs of a
+// graph near its percolation point): lane = slot, the first lane holding a
+// node discovers it (__match_any_sync), ballots keep slot order.  The level
+// is read from and written to region 0 of the global level arrays, so block
+// and grid expansions can follow.  All threads call it; returns the count.
+template <class Nbr>
+__device__ __forceinline__ int expand_warp(int token, const int* from, int items, int K, Nbr nbr, int* vis,
+                                           int* out, int* out_cnt, long long* out_seg, int* s_cnt)
+{
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        int x = -1;
+        if (lane < items) {
+            x = nbr(ld_cg(from + lane / K), lane % K);
+            if (x >= 0 && ld_cg(vis + x) == token) x = -1;
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, x >= 0 ? x : -1 - lane);
+        const bool win = x >= 0 && lane == __ffs(peers) - 1;
+        const unsigned wins = __ballot_sync(0xffffffffu, win);
+        if (win) {
+            out[__popc(wins & ((1u << lane) - 1u))] = x;
+            vis[x] = token;
+        }
+        if (lane == 0) {
+            *out_cnt = __popc(wins);
+            *out_seg = items;
+            *s_cnt = __popc(wins);
+        }
+    }
+    __syncthreads();
+    return *s_cnt;
+}
+
 // One edge, one cooperative launch:
 //  1. block 0 attaches the previous edge's winner (it owns the candidate
 //     sequence the previous summary left) and runs the BFS from v while its
@@ -345,17 +378,26 @@ __global__ void __launch_bounds__(PB) peg_step_kernel(PegArgs A, int v, int toke
                 *A.fr_seg = 1;
                 A.sum->t_pre = 0;
             }
-            for (int b = 1 + threadIdx.x; b < (int)gridDim.x; b += PB) A.fr_cnt[b] = 0;
+            for (int b = 1 + threadIdx.x; b < (int)gridDim.x; b += PB) {
+                A.fr_cnt[b] = 0;   // small levels live in region 0 only
+                A.lvl_cnt[b] = 0;
+            }
             __syncthreads();
             int nF = 1, nL = 0, reached = 0, hl = 0, stage = 0, done = 0;
             for (;;) {
                 if (stage == 0) {
                     const long long items = (long long)nF * KV;
                     if (items > kSmallLevel) break;
-                    F.seg = ld_cg(A.fr_seg);
-                    F.total = load_prefix(A.fr_cnt, s_pre, sh);
-                    expand(A, token, hl, F, KV, nbr_v2c, A.key_c, A.vis_c, A.lvl, A.lvl_cnt, A.lvl_seg, false, sh);
-                    nL = ld_cg(A.lvl_cnt);
+                    if (items <= 32) {
+                        nL = expand_warp(token, A.fr, (int)items, KV, nbr_v2c, A.vis_c, A.lvl, A.lvl_cnt, A.lvl_seg,
+                                         &s_i[2 * ND + 1]);
+                    } else {
+                        F.seg = ld_cg(A.fr_seg);
+                        F.total = load_prefix(A.fr_cnt, s_pre, sh);
+                        expand(A, token, hl, F, KV, nbr_v2c, A.key_c, A.vis_c, A.lvl, A.lvl_cnt, A.lvl_seg, false,
+                               sh);
+                        nL = ld_cg(A.lvl_cnt);
+                    }
                     ++hl;
                     if (nL == 0) { done = 1; break; }
                     reached += nL;
@@ -364,10 +406,15 @@ __global__ void __launch_bounds__(PB) peg_step_kernel(PegArgs A, int v, int toke
                 } else {
                     const long long items = (long long)nL * kc;
                     if (items > kSmallLevel) break;
-                    L.seg = ld_cg(A.lvl_seg);
-                    L.total = load_prefix(A.lvl_cnt, s_pre, sh);
-                    expand(A, token, hl, L, kc, nbr_c2v, A.key_v, A.vis_v, A.fr, A.fr_cnt, A.fr_seg, false, sh);
-                    nF = ld_cg(A.fr_cnt);
+                    if (items <= 32) {
+                        nF = expand_warp(token, A.lvl, (int)items, kc, nbr_c2v, A.vis_v, A.fr, A.fr_cnt, A.fr_seg,
+                                         &s_i[2 * ND + 1]);
+                    } else {
+                        L.seg = ld_cg(A.lvl_seg);
+                        L.total = load_prefix(A.lvl_cnt, s_pre, sh);
+                        expand(A, token, hl, L, kc, nbr_c2v, A.key_v, A.vis_v, A.fr, A.fr_cnt, A.fr_seg, false, sh);
+                        nF = ld_cg(A.fr_cnt);
+                    }
                     ++hl;
                     if (nF == 0) { done = 1; break; }
                     stage = 0;
@@ -566,11 +613,21 @@ struct DevMem {
 
 }  // namespace
 
-int mbp_peg_build_device(int32_t n, int32_t m, const int32_t* col_deg, uint64_t seed, int64_t* chk_ptr,
-                         int32_t* chk_var, int device)
+namespace {
+
+// Variables [v_begin, v_end) of the construction on GPU `device`.  vn_adj
+// (host, [n][KV], -1 = no edge) holds the graph of variables < v_begin in
+// edge order and receives the rows up to v_end; *state is the tie-break
+// stream's state at v_begin (derived from `seed` when v_begin == 0) and at
+// v_end on return.  Check rows list their variables in attachment order,
+// which is ascending variable order, so the device graph is rebuilt from
+// vn_adj alone: a construction can stop and resume anywhere.
+int peg_device_run(int32_t n, int32_t m, const int32_t* col_deg, uint64_t seed, uint64_t* state_io, int32_t v_begin,
+                   int32_t v_end, int32_t* vn_adj_host, int device)
 {
-    if (!col_deg || !chk_ptr || !chk_var) return mbp::set_error(MBP_EINVAL, "null pointer argument");
+    if (!col_deg || !vn_adj_host || !state_io) return mbp::set_error(MBP_EINVAL, "null pointer argument");
     if (!(0 < m && m < n)) return mbp::set_error(MBP_EINVAL, "need 0 < m < n");
+    if (v_begin < 0 || v_end < v_begin || v_end > n) return mbp::set_error(MBP_EINVAL, "bad variable range");
     int64_t E = 0;
     for (int i = 0; i < n; ++i) {
         if (col_deg[i] < 1 || col_deg[i] > std::min(m, KV))
@@ -580,6 +637,21 @@ int mbp_peg_build_device(int32_t n, int32_t m, const int32_t* col_deg, uint64_t 
     if (E >= (1 << 22)) return mbp::set_error(MBP_EUNSUPPORTED, "device PEG supports < 2^22 edges");
     if ((long long)n * KV >= (1 << 24) || (long long)m * KC >= (1 << 24))
         return mbp::set_error(MBP_EUNSUPPORTED, "device PEG supports n < 2^22 and m < 2^20");
+    // the graph so far, rebuilt on the host
+    std::vector<int> vdeg(n, 0), cdeg(m, 0), cadj((size_t)m * KC, -1);
+    int kc = 1;   // effective check-adjacency slots: the largest check degree so far
+    for (int v = 0; v < v_begin; ++v) {
+        for (int k = 0; k < KV; ++k) {
+            const int c = vn_adj_host[(size_t)v * KV + k];
+            if (c < 0) break;
+            if (c >= m || k >= col_deg[v]) return mbp::set_error(MBP_EINVAL, "resume graph does not fit (n, m, degrees)");
+            if (cdeg[c] >= KC) return mbp::set_error(MBP_EUNSUPPORTED, "resume graph exceeds the check capacity");
+            cadj[(size_t)c * KC + cdeg[c]++] = v;
+            kc = std::max(kc, cdeg[c]);
+            vdeg[v] = k + 1;
+        }
+        if (vdeg[v] != col_deg[v]) return mbp::set_error(MBP_EINVAL, "resume graph: a variable before v_begin is incomplete");
+    }
     int prev_dev = 0;
     cudaGetDevice(&prev_dev);
     PEG_CUDA(cudaSetDevice(device));
@@ -599,6 +671,10 @@ int mbp_peg_build_device(int32_t n, int32_t m, const int32_t* col_deg, uint64_t 
     PEG_CUDA(mem.alloc(&A.vn_deg, n, 0));
     PEG_CUDA(mem.alloc(&A.cn_adj, (size_t)m * KC, 0xff));
     PEG_CUDA(mem.alloc(&A.cn_deg, m, 0));
+    PEG_CUDA(cudaMemcpy(A.vn_adj, vn_adj_host, sizeof(int) * (size_t)n * KV, cudaMemcpyHostToDevice));
+    PEG_CUDA(cudaMemcpy(A.vn_deg, vdeg.data(), sizeof(int) * n, cudaMemcpyHostToDevice));
+    PEG_CUDA(cudaMemcpy(A.cn_adj, cadj.data(), sizeof(int) * (size_t)m * KC, cudaMemcpyHostToDevice));
+    PEG_CUDA(cudaMemcpy(A.cn_deg, cdeg.data(), sizeof(int) * m, cudaMemcpyHostToDevice));
     PEG_CUDA(mem.alloc(&A.vis_c, m, 0));
     PEG_CUDA(mem.alloc(&A.vis_v, n, 0));
     PEG_CUDA(mem.alloc(&A.key_c, m, 0xff));
@@ -627,8 +703,11 @@ int mbp_peg_build_device(int32_t n, int32_t m, const int32_t* col_deg, uint64_t 
     struct FreeStream { cudaStream_t s; ~FreeStream() { cudaStreamDestroy(s); } } fs{s};
 
     DivTab dt((size_t)m + 2);
-    uint64_t state = splitmix64(seed);
-    if (state == 0) state = 0x9E3779B97F4A7C15ull;
+    uint64_t state = *state_io;
+    if (v_begin == 0) {
+        state = splitmix64(seed);
+        if (state == 0) state = 0x9E3779B97F4A7C15ull;
+    }
     const int debug = std::getenv("MBP_PEG_DEBUG") ? std::atoi(std::getenv("MBP_PEG_DEBUG")) : 0;
     double t_rng = 0.0, t_wait = 0.0;
     unsigned long long draws = 0;
@@ -637,14 +716,13 @@ int mbp_peg_build_device(int32_t n, int32_t m, const int32_t* col_deg, uint64_t 
     int token = 0;
     int attach_v = -1;
     unsigned long long attach_j = 0;
-    int kc = 1;   // effective check-adjacency slots: the largest check degree so far
     auto launch = [&](int v, int tok, int do_bfs) -> cudaError_t {
         void* args[] = {(void*)&A, (void*)&v, (void*)&tok, (void*)&attach_v, (void*)&attach_j, (void*)&do_bfs,
                         (void*)&kc};
         return cudaLaunchCooperativeKernel((const void*)peg_step_kernel, dim3(grid), dim3(PB), args, 0, s);
     };
-    for (int v = 0; v < n; ++v) {
-        if (debug >= 2 && v && (v & 0xffff) == 0)
+    for (int v = v_begin; v < v_end; ++v) {
+        if (debug >= 2 && v > v_begin && (v & 0xffff) == 0)
             fprintf(stderr, "peg_gpu seed=%llu: %d/%d variables, %.0f s, %.1f s GPU, %.1f s stream\n",
                     (unsigned long long)seed, v, n, std::chrono::duration<double>(now() - t_start).count(), t_wait,
                     t_rng);
@@ -678,21 +756,50 @@ int mbp_peg_build_device(int32_t n, int32_t m, const int32_t* col_deg, uint64_t 
         }
     }
     if (debug >= 2)
-        fprintf(stderr, "peg_gpu n=%d m=%d seed=%llu: %.1f s total, %.1f s waiting for the GPU (%.1f us/edge), "
+        fprintf(stderr, "peg_gpu n=%d m=%d seed=%llu [%d, %d): %.1f s total, %.1f s waiting for the GPU (%.1f us/edge), "
                         "%.1f s tie-break stream (%.3e draws, %.2f ns/draw)\n",
-                n, m, (unsigned long long)seed, std::chrono::duration<double>(now() - t_start).count(), t_wait,
-                1e6 * t_wait / std::max(1, token), t_rng, (double)draws, 1e9 * t_rng / std::max(1.0, (double)draws));
-    PEG_CUDA(launch(0, token + 1, 0));
-    PEG_CUDA(cudaMemcpyAsync(hs, A.sum, sizeof(PegSummary), cudaMemcpyDeviceToHost, s));
-    std::vector<int> cdeg(m), cadj((size_t)m * KC);
-    PEG_CUDA(cudaMemcpyAsync(cdeg.data(), A.cn_deg, sizeof(int) * m, cudaMemcpyDeviceToHost, s));
-    PEG_CUDA(cudaMemcpyAsync(cadj.data(), A.cn_adj, sizeof(int) * (size_t)m * KC, cudaMemcpyDeviceToHost, s));
+                n, m, (unsigned long long)seed, v_begin, v_end, std::chrono::duration<double>(now() - t_start).count(),
+                t_wait, 1e6 * t_wait / std::max(1, token), t_rng, (double)draws,
+                1e9 * t_rng / std::max(1.0, (double)draws));
+    if (attach_v >= 0) {   // the last edge's winner
+        PEG_CUDA(launch(0, token + 1, 0));
+        PEG_CUDA(cudaMemcpyAsync(hs, A.sum, sizeof(PegSummary), cudaMemcpyDeviceToHost, s));
+    }
+    PEG_CUDA(cudaMemcpyAsync(vn_adj_host, A.vn_adj, sizeof(int) * (size_t)n * KV, cudaMemcpyDeviceToHost, s));
     PEG_CUDA(cudaStreamSynchronize(s));
     if (hs->overflow) return mbp::set_error(MBP_EUNSUPPORTED, "a check exceeded the device PEG's degree capacity");
-    chk_ptr[0] = 0;
-    for (int c = 0; c < m; ++c) {
-        chk_ptr[c + 1] = chk_ptr[c] + cdeg[c];
-        std::memcpy(chk_var + chk_ptr[c], cadj.data() + (size_t)c * KC, sizeof(int) * cdeg[c]);
-    }
-    return chk_ptr[m] == E ? MBP_OK : mbp::set_error(MBP_EINVAL, "internal: edge count mismatch");
+    *state_io = state;
+    return MBP_OK;
+}
+
+}  // namespace
+
+int mbp_peg_build_device_range(int32_t n, int32_t m, const int32_t* col_deg, uint64_t seed, uint64_t* state,
+                               int32_t v_begin, int32_t v_end, int32_t* vn_adj, int device)
+{
+    return peg_device_run(n, m, col_deg, seed, state, v_begin, v_end, vn_adj, device);
+}
+
+int mbp_peg_build_device(int32_t n, int32_t m, const int32_t* col_deg, uint64_t seed, int64_t* chk_ptr,
+                         int32_t* chk_var, int device)
+{
+    if (!chk_ptr || !chk_var) return mbp::set_error(MBP_EINVAL, "null pointer argument");
+    if (!(0 < n)) return mbp::set_error(MBP_EINVAL, "need 0 < m < n");
+    std::vector<int32_t> vadj((size_t)n * KV, -1);
+    uint64_t state = 0;
+    int rc = peg_device_run(n, m, col_deg, seed, &state, 0, n, vadj.data(), device);
+    if (rc) return rc;
+    // check rows in attachment order = ascending variable order
+    std::vector<int64_t> cnt(m + 1, 0);
+    for (size_t i = 0; i < vadj.size(); ++i)
+        if (vadj[i] >= 0) ++cnt[vadj[i] + 1];
+    for (int c = 0; c < m; ++c) cnt[c + 1] += cnt[c];
+    for (int c = 0; c <= m; ++c) chk_ptr[c] = cnt[c];
+    std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+    for (int v = 0; v < n; ++v)
+        for (int k = 0; k < KV; ++k) {
+            const int c = vadj[(size_t)v * KV + k];
+            if (c >= 0) chk_var[fill[c]++] = v;
+        }
+    return MBP_OK;
 }

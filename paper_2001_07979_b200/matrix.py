@@ -214,6 +214,36 @@ def peg_construct(n: int, m: int, column_degree=3, seed: int = 0, device: int | 
     return ParityCheckMatrix._from_csr(n, m, chk_ptr, chk_var)
 
 
+def peg_device_stage(n: int, m: int, column_degree, seed: int, state: int, v_begin: int, v_end: int,
+                     vn_adj: np.ndarray, device: int = 0) -> int:
+    """One stage of the device PEG (mbp_peg_build_device_range): variables
+    [v_begin, v_end) on top of ``vn_adj`` (int32 [n, 4], -1 = no edge; updated
+    in place).  Returns the tie-break stream state at v_end (pass it to the
+    next stage); ``state`` is ignored when v_begin == 0."""
+    import ctypes as C
+
+    from . import _native as N
+
+    deg = (np.full(n, int(column_degree), dtype=np.int32) if np.ndim(column_degree) == 0
+           else np.ascontiguousarray(column_degree, dtype=np.int32))
+    if vn_adj.dtype != np.int32 or vn_adj.shape != (n, 4) or not vn_adj.flags.c_contiguous:
+        raise ValueError("vn_adj must be a contiguous int32 array of shape (n, 4)")
+    st = C.c_uint64(int(state) & 0xFFFFFFFFFFFFFFFF)
+    N.call("mbp_peg_build_device_range", int(n), int(m), deg.ctypes.data, C.c_uint64(int(seed) & 0xFFFFFFFFFFFFFFFF),
+           C.byref(st), int(v_begin), int(v_end), vn_adj.ctypes.data, int(device))
+    return int(st.value)
+
+
+def matrix_from_variable_rows(n: int, m: int, vn_adj: np.ndarray) -> ParityCheckMatrix:
+    """The PEG matrix from per-variable check lists (check rows in ascending
+    variable order, as the construction attaches them)."""
+    v, k = np.nonzero(vn_adj >= 0)
+    c = vn_adj[v, k].astype(np.int64)
+    order = np.lexsort((v, c))
+    chk_ptr = np.concatenate([[0], np.cumsum(np.bincount(c, minlength=m))]).astype(np.int64)
+    return ParityCheckMatrix._from_csr(n, m, chk_ptr, v[order].astype(np.int32))
+
+
 def build_ensemble(n: int, m: int, column_degree=3, u: int = 1, base_seed: int = 0,
                    workers: int | None = None, device: int | None = None) -> "MatrixEnsemble":
     """u PEG matrices from seeds base_seed..base_seed+u-1, as the reference's

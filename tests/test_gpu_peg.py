@@ -31,3 +31,17 @@ def test_device_peg_equals_host_peg_irregular(n, m, seed):
     a = peg_construct(n, m, deg, seed=seed)
     b = peg_construct(n, m, deg, seed=seed, device=0)
     assert a.content_hash() == b.content_hash()
+
+
+def test_staged_device_peg_equals_one_shot():
+    """mbp_peg_build_device_range chained over [0, n) in uneven stages gives
+    the one-shot matrix (the cfg 4 build checkpoints this way)."""
+    from paper_2001_07979_b200.matrix import matrix_from_variable_rows, peg_device_stage
+
+    n, m, seed = 4096, 2048, 1
+    rows = np.full((n, 4), -1, dtype=np.int32)
+    state = 0
+    for lo, hi in ((0, 1000), (1000, 1001), (1001, 3333), (3333, n)):
+        state = peg_device_stage(n, m, 3, seed, state, lo, hi, rows, 0)
+    staged = matrix_from_variable_rows(n, m, rows)
+    assert staged.content_hash() == peg_construct(n, m, 3, seed=seed).content_hash()
