@@ -548,6 +548,21 @@ __device__ __forceinline__ void sc_var1_chunk(const ScatterArgs& A, const SL<CPT
         }
     }
     __syncwarp();
+#ifndef MBP_V1_UNI
+#define MBP_V1_UNI 1
+#endif
+    // variables whose checks all have one degree d (95 % of cfg 2's): the
+    // sum of +-M_d is M_d * (DV - 2 * #mismatches) -- one table read instead
+    // of a dependent (degree, table) pair per edge; the same integer
+    int8_t* s_uni = reinterpret_cast<int8_t*>(s_deg + 32 * 9);
+    if (MBP_V1_UNI && lane < rows) {
+        const int d0 = s_deg[lane * DV];
+        bool same = true;
+#pragma unroll
+        for (int k = 1; k < DV; ++k) same &= s_deg[lane * DV + k] == d0;
+        s_uni[lane] = same ? (int8_t)d0 : (int8_t)-1;
+    }
+    __syncwarp();
     int r = 0;
     while (r < rows) {
         const int item = base + r;
@@ -572,13 +587,20 @@ __device__ __forceinline__ void sc_var1_chunk(const ScatterArgs& A, const SL<CPT
                 for (; v + UV - 1 < r + span; v += UV) {
                     int a[UV];
 #pragma unroll
-                    for (int q = 0; q < UV; ++q) a[q] = Lf;
+                    for (int q = 0; q < UV; ++q) {
+                        const int du = MBP_V1_UNI ? (int)s_uni[v + q] : -1;
+                        if (du >= 0) {
+                            int cnt = 0;
 #pragma unroll
-                    for (int k = 0; k < DV; ++k) {
+                            for (int k = 0; k < DV; ++k) cnt += (s_mis[(v + q) * DV + k] >> lane) & 1u;
+                            a[q] = Lf + s_mf[du * 32 + lane] * (DV - 2 * cnt);
+                        } else {
+                            a[q] = Lf;
 #pragma unroll
-                        for (int q = 0; q < UV; ++q) {
-                            const int mq = s_mf[s_deg[(v + q) * DV + k] * 32 + lane];
-                            a[q] += (s_mis[(v + q) * DV + k] & lbit) ? -mq : mq;
+                            for (int k = 0; k < DV; ++k) {
+                                const int mq = s_mf[s_deg[(v + q) * DV + k] * 32 + lane];
+                                a[q] += (s_mis[(v + q) * DV + k] & lbit) ? -mq : mq;
+                            }
                         }
                     }
                     const size_t w = (size_t)base + v;
@@ -957,7 +979,7 @@ __global__ void __launch_bounds__(kDecodeThreads, scatter_min_blocks<D>()) decod
     // lane's sweep-1 magnitude per degree
     constexpr int V1 = D <= 16 ? 32 * 9 : 0;
     constexpr int M1T = D <= 16 ? (D + 1) * 32 : 0;
-    constexpr int RAW = (V1 + V1 / 4) > M1T ? (V1 + V1 / 4) + 1 : M1T + 1;
+    constexpr int RAW = (V1 + V1 / 4 + 8) > M1T ? (V1 + V1 / 4 + 8) + 1 : M1T + 1;   // + per-variable uniform degree
     __shared__ unsigned s_raw_all[kDecodeThreads / 32][RAW];
     int* s_idx = s_idx_all[warp];
     unsigned* s_w = s_w_all[warp];
