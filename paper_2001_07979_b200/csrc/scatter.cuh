@@ -162,7 +162,7 @@ struct SL {
 // integer, ties to even, when |c * 2^S| < 2^22 -- the kernel caps S for
 // that) instead of F2I, which issues on the XU pipe next to the rule's MUFUs.
 #ifndef MBP_FIX_MAGIC
-#define MBP_FIX_MAGIC 1
+#define MBP_FIX_MAGIC 0   // off: the 2^-16 resolution it forces changes failing frames' final states (measured)
 #endif
 __device__ __forceinline__ int fixq(float c, float scale)
 {
@@ -549,7 +549,7 @@ __device__ __forceinline__ void sc_var1_chunk(const ScatterArgs& A, const SL<CPT
     }
     __syncwarp();
 #ifndef MBP_V1_UNI
-#define MBP_V1_UNI 1
+#define MBP_V1_UNI 0   // off: no gain measured (the phase is latency-bound, not issue-bound)
 #endif
     // variables whose checks all have one degree d (95 % of cfg 2's): the
     // sum of +-M_d is M_d * (DV - 2 * #mismatches) -- one table read instead
@@ -580,7 +580,7 @@ __device__ __forceinline__ void sc_var1_chunk(const ScatterArgs& A, const SL<CPT
             if (act == kFull && !A.hist_w) {
                 // every lane live, no history: UV variables per pass, no predicates
 #ifndef MBP_V1_UV
-#define MBP_V1_UV 2
+#define MBP_V1_UV 4
 #endif
                 constexpr int UV = MBP_V1_UV;
                 int v = r;
