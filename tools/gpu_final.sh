@@ -20,6 +20,9 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:deco
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct \
   --clock-control none -k regex:decode_scatter -c 2 --csv --log-file gpurun_out/${TAG}_dram_cfg3.csv \
   python tools/profile_decode.py --cfg cfg3 --frames 1024 --once > /dev/null 2>&1; echo "ncu cfg3 rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct \
+  --clock-control none -k regex:decode_scatter -c 1 --csv --log-file gpurun_out/${TAG}_dram_cfg4.csv \
+  python tools/profile_decode.py --cfg cfg4 --frames 1024 --once > /dev/null 2>&1; echo "ncu cfg4 rc=$?"
 if [ "${SAN:-1}" = "1" ]; then
   timeout 900 compute-sanitizer --tool memcheck --print-limit 50 python tools/sanitize_run.py > gpurun_out/${TAG}_san_memcheck.log 2>&1; echo "memcheck rc=$?"; tail -2 gpurun_out/${TAG}_san_memcheck.log
 fi
