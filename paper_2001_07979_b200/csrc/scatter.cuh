@@ -75,7 +75,10 @@ constexpr int kVB = 96;         // 32-bit words per variable block (3 lines)
 // 3.4 KB, D = 14 2.0 KB of spill stores, mostly cold paths: the explicit-base
 // and saturation variants); measured trade-off in DESIGN.md §10
 template <int D>
-constexpr int scatter_min_blocks() { return D <= 8 ? MBP_SCATTER_MIN_BLOCKS : 2; }
+#ifndef MBP_WIDE_MIN_BLOCKS
+#define MBP_WIDE_MIN_BLOCKS 2
+#endif
+constexpr int scatter_min_blocks() { return D <= 8 ? MBP_SCATTER_MIN_BLOCKS : MBP_WIDE_MIN_BLOCKS; }
 
 struct ScatterArgs {
     // graph
@@ -752,6 +755,52 @@ __device__ __forceinline__ int sc_syncheck_item(const ScatterArgs& A, const SL<C
     return __any_sync(kFull, mism != 0) ? __popc(warp_transpose32(mism, lane)) : 0;
 }
 
+// Two items of one group at once (MBP_SYN_PAIR): the rows' id and
+// hard-word loads are issued together, so each lane has twice the loads in
+// flight through the two dependent rounds (ids, then words).
+template <int D, bool CPT>
+__device__ __forceinline__ int sc_syncheck_pair(const ScatterArgs& A, const SL<CPT>& S, int g, int blk, int t,
+                                                unsigned act, int lane)
+{
+    constexpr int DU = D < 16 ? D : 16;
+    const int j0 = blk * 32 + lane, j1 = j0 + 32;
+    const bool v0 = j0 < A.C, v1 = j1 < A.C;
+    const unsigned* hw = S.hard_w() + (size_t)g * A.n;
+    const int d0 = v0 ? ld_ro(A.deg + j0) : 0, d1 = v1 ? ld_ro(A.deg + j1) : 0;
+    const int* r0 = A.chk_ell + (size_t)j0 * A.Ds;
+    const int* r1 = A.chk_ell + (size_t)j1 * A.Ds;
+    unsigned p0 = 0, p1 = 0;
+    const int dm = max(d0, d1);
+    for (int k0 = 0; k0 < dm; k0 += DU) {
+        int a[DU], b[DU];
+#pragma unroll
+        for (int k = 0; k < DU; ++k) {
+            a[k] = k0 + k < d0 ? ld_ro(r0 + k0 + k) : -1;
+            b[k] = k0 + k < d1 ? ld_ro(r1 + k0 + k) : -1;
+        }
+#pragma unroll
+        for (int k = 0; k < DU; ++k) {
+            if (a[k] >= 0) p0 ^= ld_cg(hw + a[k]);
+            if (b[k] >= 0) p1 ^= ld_cg(hw + b[k]);
+        }
+    }
+    unsigned m0 = 0, m1 = 0;
+    if (v0) {
+        const unsigned full = p0 ^ S.syn((size_t)g * A.C + j0);
+        if (t == 0) S.mis()[(size_t)g * A.C + j0] = full;
+        m0 = full & act;
+    }
+    if (v1) {
+        const unsigned full = p1 ^ S.syn((size_t)g * A.C + j1);
+        if (t == 0) S.mis()[(size_t)g * A.C + j1] = full;
+        m1 = full & act;
+    }
+    int c = 0;
+    if (__any_sync(kFull, m0 != 0)) c += __popc(warp_transpose32(m0, lane));
+    if (__any_sync(kFull, m1 != 0)) c += __popc(warp_transpose32(m1, lane));
+    return c;
+}
+
 // items per claim: about one claim per warp (few flushes per group line),
 // at least 8 so small batches do not spread thin
 __device__ __forceinline__ int syn_chunk(int total, int nwarps)
@@ -768,7 +817,10 @@ __device__ __forceinline__ void sc_syncheck_chunk(const ScatterArgs& A, const SL
     unsigned act = cprev ? group_mask(cprev, g, lane) : kFull;
     int c = 0;
     bool bad = false;
-    for (int item = base; item < end; ++item) {
+#ifndef MBP_SYN_PAIR
+#define MBP_SYN_PAIR 1
+#endif
+    for (int item = base; item < end;) {
         const int gi = item / cblk;
         if (gi != g) {
             if (c) atomicAdd(S.cnt() + (t & 1) * S.G * 32 + g * 32 + lane, c);
@@ -777,7 +829,12 @@ __device__ __forceinline__ void sc_syncheck_chunk(const ScatterArgs& A, const SL
             g = gi;
             act = cprev ? group_mask(cprev, g, lane) : kFull;
         }
-        if (act) c += sc_syncheck_item<D, CPT>(A, S, g, item - g * cblk, t, act, lane);
+        const bool pair = MBP_SYN_PAIR && item + 1 < end && (item + 1) / cblk == g;
+        if (act) {
+            if (pair) c += sc_syncheck_pair<D, CPT>(A, S, g, item - g * cblk, t, act, lane);
+            else c += sc_syncheck_item<D, CPT>(A, S, g, item - g * cblk, t, act, lane);
+        }
+        item += pair ? 2 : 1;
     }
     if (c) atomicAdd(S.cnt() + (t & 1) * S.G * 32 + g * 32 + lane, c);
     bad |= c != 0;

@@ -22,11 +22,16 @@ syn_d = dec.syndromes(torch.from_numpy(fb.keys).to(dev))
 noisy_d = torch.from_numpy(fb.noisy).to(dev)
 pin_noisy = torch.from_numpy(fb.noisy).pin_memory().numpy()
 pin_syn = syn_d.cpu().pin_memory().numpy()
+from paper_2001_07979_b200.decoder import BatchResult  # noqa: E402
+
+pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
+out = BatchResult(pin(np.empty_like(fb.noisy)), pin(np.empty(B, np.uint8)), pin(np.empty(B, np.int32)),
+                  pin(np.empty(B, np.int32)), ens.n)
 for sub in ("1", "2", "3", "4", "6", "8"):
     os.environ["MBP_HOST_SUBBATCHES"] = sub
     ts = []
     for k in range(6):
-        dec.decode(pin_noisy, pin_syn, 0.03)
+        dec.decode(pin_noisy, pin_syn, 0.03, out=out)
         if k >= 2:
             ts.append(dec.last_timing(e2e=True)[1])
     print(f"subbatches {sub}: e2e {np.mean(ts):.3f} ms  ({B * ens.n / np.mean(ts) / 1e6:.0f} Mbps)")
