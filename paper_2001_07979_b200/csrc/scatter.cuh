@@ -376,7 +376,10 @@ __device__ __forceinline__ void sc_span(const ScatterArgs& A, const SL<CPT>& S, 
     // two rows per loop pass for the narrow (64-register) instances: the
     // prefetch buffers alternate instead of being copied; wide rows keep one
     // (their 128-register budget is taken by the two-row chain prefetch)
-    constexpr int UR = D <= 8 ? kSpanUnroll : 1;
+#ifndef MBP_C3_UR
+#define MBP_C3_UR 1   // the two-rule sweep-3 rows: one row per pass (registers for the chain)
+#endif
+    constexpr int UR = D <= 8 ? (C3 ? MBP_C3_UR : kSpanUnroll) : 1;
 #pragma unroll (UR)
     for (int r = r0; r < r1; ++r) {
         float p[D], p2[D];
@@ -459,7 +462,10 @@ __device__ __forceinline__ void sc_check_chunk(const ScatterArgs& A, const SL<CP
                 if (t == 2)
                     sc_span<D, false, true, CPT>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d, s_m1, first,
                                                  scale);
-                else if (t == 3 && kStoreFrom == 3)
+#ifndef MBP_C3
+#define MBP_C3 1
+#endif
+                else if (MBP_C3 && t == 3 && kStoreFrom == 3)
                     sc_span<D, false, false, CPT, true>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d, s_m1,
                                                         first, scale);
                 else
