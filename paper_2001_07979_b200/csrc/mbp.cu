@@ -539,6 +539,49 @@ static __global__ void gather_rel_post_kernel(const float* __restrict__ vb_g, co
     }
 }
 
+// The per-chunk control state (counters, flags, slot maps) reset by one
+// launch instead of a dozen small memsets.
+struct FillSpan {
+    unsigned* p;
+    long long words;
+    unsigned v;
+};
+struct FillArgs {
+    FillSpan s[12];
+    int n;
+};
+
+static __global__ void fill_spans_kernel(FillArgs a)
+{
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x, st = (long long)gridDim.x * blockDim.x;
+    for (int k = 0; k < a.n; ++k)
+        for (long long i = t; i < a.s[k].words; i += st) a.s[k].p[i] = a.s[k].v;
+}
+
+static int reset_chunk_state(mbp_workspace* ws, int F, cudaStream_t s, bool lmax)
+{
+    FillArgs a{};
+    auto add = [&](const DevBuf& b, size_t bytes, unsigned v) {
+        if (bytes) a.s[a.n++] = FillSpan{(unsigned*)b.p, (long long)(bytes / 4), v};
+    };
+    add(ws->cnt, 2 * (size_t)F * 4, 0u);
+    add(ws->any_bad, 8, 0u);
+    add(ws->iters, (size_t)F * 4, ~0u);
+    add(ws->barrier, 8, 0u);
+    add(ws->work, ws->work.bytes, 0u);
+    add(ws->sweeps, 8, 0u);
+    if (ws->Gb) {
+        add(ws->ctrl, ws->ctrl.bytes, 0u);
+        add(ws->fid_b, ws->fid_b.bytes, ~0u);
+        add(ws->src_b, ws->src_b.bytes, ~0u);
+        add(ws->newslot, ws->newslot.bytes, ~0u);
+    }
+    if (lmax) add(ws->sc_Lmax, 4, 0u);
+    fill_spans_kernel<<<64, 256, 0, s>>>(a);
+    MBP_CUDA(cudaGetLastError());
+    return MBP_OK;
+}
+
 // Scatter path (scatter.cuh) for one chunk of <= ws->cap frames.
 static int decode_chunk_scatter(mbp_workspace* ws, const uint8_t* noisy, const uint8_t* syn, const double* e,
                                 int e_stride, int B, uint8_t* corrected, uint8_t* conv, int* iters, int* mism,
@@ -551,7 +594,7 @@ static int decode_chunk_scatter(mbp_workspace* ws, const uint8_t* noisy, const u
     const int Dm = ens->Ds;
     int rc;
     // tables are laid out with the chunk's own frame stride F = 32 G
-    MBP_CUDA(cudaMemsetAsync(ws->sc_Lmax.p, 0, 4, s));
+    if ((rc = reset_chunk_state(ws, F, s, true))) return rc;
     mbp::scatter_setup_kernel<<<(F + 127) / 128, 128, 0, s>>>(e, e_stride, B, F, Dm, (double)(float)cfg.llr_clamp,
                                                                ws->Lmag.as<float>(), ws->sc_Mtab.as<float>(),
                                                                ws->sc_Lmax.as<float>());
@@ -570,18 +613,6 @@ static int decode_chunk_scatter(mbp_workspace* ws, const uint8_t* noisy, const u
         // that stop at iteration 0
         fill_rel_prior_kernel<<<1024, 256, 0, s>>>(ws->Lmag.as<float>(), G, ens->n, ws->sc_vb.as<float>());
         MBP_CUDA(cudaGetLastError());
-    }
-    MBP_CUDA(cudaMemsetAsync(ws->cnt.p, 0, 2 * (size_t)F * 4, s));
-    MBP_CUDA(cudaMemsetAsync(ws->any_bad.p, 0, 8, s));
-    MBP_CUDA(cudaMemsetAsync(ws->iters.p, 0xff, (size_t)F * 4, s));
-    MBP_CUDA(cudaMemsetAsync(ws->barrier.p, 0, 8, s));
-    MBP_CUDA(cudaMemsetAsync(ws->work.p, 0, ws->work.bytes, s));
-    MBP_CUDA(cudaMemsetAsync(ws->sweeps.p, 0, 8, s));
-    if (ws->Gb) {
-        MBP_CUDA(cudaMemsetAsync(ws->ctrl.p, 0, ws->ctrl.bytes, s));
-        MBP_CUDA(cudaMemsetAsync(ws->fid_b.p, 0xff, ws->fid_b.bytes, s));
-        MBP_CUDA(cudaMemsetAsync(ws->src_b.p, 0xff, ws->src_b.bytes, s));
-        MBP_CUDA(cudaMemsetAsync(ws->newslot.p, 0xff, ws->newslot.bytes, s));
     }
     mbp::ScatterArgs A;
     std::memset(&A, 0, sizeof A);
@@ -652,18 +683,7 @@ static int decode_chunk(mbp_workspace* ws, const uint8_t* noisy, const uint8_t* 
         MBP_CUDA(cudaGetLastError());
         MBP_CUDA(cudaMemsetAsync(ws->c2v.p, 0, (size_t)G * ens->C * ens->Ds * 32 * sizeof(Real), s));
     }
-    MBP_CUDA(cudaMemsetAsync(ws->cnt.p, 0, 2 * (size_t)F * 4, s));
-    MBP_CUDA(cudaMemsetAsync(ws->any_bad.p, 0, 8, s));
-    MBP_CUDA(cudaMemsetAsync(ws->iters.p, 0xff, (size_t)F * 4, s));
-    MBP_CUDA(cudaMemsetAsync(ws->barrier.p, 0, 8, s));
-    MBP_CUDA(cudaMemsetAsync(ws->work.p, 0, ws->work.bytes, s));
-    MBP_CUDA(cudaMemsetAsync(ws->sweeps.p, 0, 8, s));
-    if (ws->Gb) {
-        MBP_CUDA(cudaMemsetAsync(ws->ctrl.p, 0, ws->ctrl.bytes, s));
-        MBP_CUDA(cudaMemsetAsync(ws->fid_b.p, 0xff, ws->fid_b.bytes, s));
-        MBP_CUDA(cudaMemsetAsync(ws->src_b.p, 0xff, ws->src_b.bytes, s));
-        MBP_CUDA(cudaMemsetAsync(ws->newslot.p, 0xff, ws->newslot.bytes, s));
-    }
+    if ((rc = reset_chunk_state(ws, F, s, false))) return rc;
 
     mbp::DecodeArgs<Real> A;
     std::memset(&A, 0, sizeof A);
