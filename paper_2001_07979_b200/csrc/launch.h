@@ -16,9 +16,10 @@ cudaError_t launch_explicit_f64(const DecodeArgs<double>& A, int D, bool damp, b
                                 cudaStream_t s);
 cudaError_t launch_explicit_f64_wide(const DecodeArgs<double>& A, int D, bool damp, bool iso, int sm_count,
                                      cudaStream_t s);   // D >= 32
-cudaError_t launch_scatter_small(const ScatterArgs& A, int D, int sm_count, cudaStream_t s);   // D 3..8
-cudaError_t launch_scatter_mid(const ScatterArgs& A, int D, int sm_count, cudaStream_t s);     // D 9..16
-cudaError_t launch_scatter_large(const ScatterArgs& A, int D, int sm_count, cudaStream_t s);   // D 20..64
+// hot = true: the hot instance of decode_scatter_kernel (D <= 16 only)
+cudaError_t launch_scatter_small(const ScatterArgs& A, int D, bool hot, int sm_count, cudaStream_t s);   // D 3..8
+cudaError_t launch_scatter_mid(const ScatterArgs& A, int D, bool hot, int sm_count, cudaStream_t s);     // D 9..16
+cudaError_t launch_scatter_large(const ScatterArgs& A, int D, int sm_count, cudaStream_t s);             // D 20..64
 
 template <class Kern, class Args>
 cudaError_t launch_coop(Kern kern, const Args& A, int sm_count, cudaStream_t s)

@@ -385,7 +385,7 @@ static int ws_alloc(mbp_workspace* ws)
         if ((rc = ws->Lmag.alloc(F * R)) || (rc = ws->noisy_w.alloc((size_t)ws->G * ens->n * 4)) ||
             (rc = ws->syn_w.alloc((size_t)ws->G * ens->C * 4)) || (rc = ws->hard_w.alloc((size_t)ws->G * ens->n * 4)) ||
             (rc = ws->cnt.alloc(2 * F * 4)) || (rc = ws->any_bad.alloc(2 * 4)) || (rc = ws->iters.alloc(F * 4)) ||
-            (rc = ws->barrier.alloc(2 * 4)) || (rc = ws->sweeps.alloc(2 * 4)))
+            (rc = ws->barrier.alloc(2 * 4)) || (rc = ws->sweeps.alloc(16 * 4)))
             return rc;
     }
     return MBP_OK;
@@ -488,14 +488,37 @@ static int dispatch_decode(mbp_workspace* ws, mbp::DecodeArgs<Real>& A, cudaStre
     return MBP_OK;
 }
 
-static int dispatch_scatter(mbp_workspace* ws, const mbp::ScatterArgs& A, cudaStream_t s)
+// Hot/tail split (scatter.cuh): the hot instance runs sweeps 1..3 and, when
+// frames remain, leaves its loop state in ws->sweeps[8..15] for the full
+// instance launched behind it (which returns at once otherwise).  Saturating
+// inputs (clamp >= sat) and wide rows run the full instance alone.
+// MBP_NO_HOT=1 in the environment forces the single full launch (A/B runs).
+static bool hot_split_enabled()
+{
+    static const bool on = [] {
+        const char* v = std::getenv("MBP_NO_HOT");
+        return !(v && std::atoi(v) != 0);
+    }();
+    return on;
+}
+
+static int dispatch_scatter(mbp_workspace* ws, mbp::ScatterArgs A, cudaStream_t s)
 {
     const int D = scatter_degree(ws->ens->Ds);
     const int sm = ws->ens->sm_count;
+    const bool split = D <= 16 && A.clamp < A.sat && hot_split_enabled();
     MBP_CUDA(cudaEventRecord(ws->ev0, s));
-    cudaError_t err = D <= 8 ? mbp::launch_scatter_small(A, D, sm, s)
-                    : D <= 16 ? mbp::launch_scatter_mid(A, D, sm, s)
-                              : mbp::launch_scatter_large(A, D, sm, s);
+    cudaError_t err = cudaSuccess;
+    A.resume = split ? ws->sweeps.as<int>() + 8 : nullptr;
+    if (split) {
+        err = D <= 8 ? mbp::launch_scatter_small(A, D, true, sm, s) : mbp::launch_scatter_mid(A, D, true, sm, s);
+        if (err == cudaSuccess)
+            err = D <= 8 ? mbp::launch_scatter_small(A, D, false, sm, s) : mbp::launch_scatter_mid(A, D, false, sm, s);
+    } else {
+        err = D <= 8 ? mbp::launch_scatter_small(A, D, false, sm, s)
+            : D <= 16 ? mbp::launch_scatter_mid(A, D, false, sm, s)
+                      : mbp::launch_scatter_large(A, D, sm, s);
+    }
     if (err == cudaErrorNotSupported) return fail(MBP_EUNSUPPORTED, "check degree too large");
     MBP_CUDA(err);
     MBP_CUDA(cudaEventRecord(ws->ev1, s));
@@ -569,7 +592,7 @@ static int reset_chunk_state(mbp_workspace* ws, int F, cudaStream_t s, bool lmax
     add(ws->iters, (size_t)F * 4, ~0u);
     add(ws->barrier, 8, 0u);
     add(ws->work, ws->work.bytes, 0u);
-    add(ws->sweeps, 8, 0u);
+    add(ws->sweeps, 16 * 4, 0u);   // sweeps_run[2] + the hot instance's resume block [8..15]
     if (ws->Gb) {
         add(ws->ctrl, ws->ctrl.bytes, 0u);
         add(ws->fid_b, ws->fid_b.bytes, ~0u);

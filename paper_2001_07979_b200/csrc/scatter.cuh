@@ -60,6 +60,7 @@
 namespace mbp {
 
 constexpr int kStoreFrom = 3;   // c2v_t is stored for t >= kStoreFrom
+constexpr int kHotSweeps = 3;   // the hot instance runs sweeps 1..kHotSweeps
 
 #ifndef MBP_SPAN_UNROLL
 #define MBP_SPAN_UNROLL 2
@@ -121,6 +122,11 @@ struct ScatterArgs {
     int* newslot;
     int* grp_cnt;
     int* ctrl;
+    // hot/tail split: the hot instance (sweeps <= kHotSweeps, no saturating
+    // inputs) stores its loop state here when frames remain; the tail
+    // instance launched after it resumes from that state or exits at once.
+    // nullptr: one full-instance launch runs the whole decode.
+    int* resume;                      // [8]: flag, t, cpt, G, tc, may_compact, wc, ts_k
     // control
     int* any_bad;
     int* iters;
@@ -423,11 +429,16 @@ __device__ __forceinline__ void sc_span(const ScatterArgs& A, const SL<CPT>& S, 
     }
 }
 
-template <int D, bool CPT>
+template <int D, bool CPT, bool HOT>
 __device__ __forceinline__ void sc_check_chunk(const ScatterArgs& A, const SL<CPT>& S, int base, int end, int t,
                                                const int* cprev, int lane, unsigned* s_off, unsigned* s_m,
                                                int* s_d, float* s_m1, bool first, float scale)
 {
+#ifndef MBP_C3
+#define MBP_C3 1
+#endif
+    static_assert(!HOT || (MBP_C3 && kStoreFrom == 3 && kHotSweeps == 3),
+                  "the hot instance runs sweeps 2 and 3 on the T2 / C3 variants only");
     constexpr int SD = Chunk<D>::SD;
     const int rows = end - base;
     if (lane < rows) {
@@ -457,21 +468,22 @@ __device__ __forceinline__ void sc_check_chunk(const ScatterArgs& A, const SL<CP
                 }
             }
             // fast variants: no input can saturate; sweeps 2 and 3 (the hot
-            // cases) compiled on their own
-            if (A.clamp < A.sat) {
+            // cases) compiled on their own.  The hot instance has only these
+            // two (the host launches it only when clamp < sat; it stops
+            // before sweep kHotSweeps + 1), which keeps the cold
+            // explicit-base and saturation code out of its register
+            // allocation
+            if (HOT || A.clamp < A.sat) {
                 if (t == 2)
                     sc_span<D, false, true, CPT>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d, s_m1, first,
                                                  scale);
-#ifndef MBP_C3
-#define MBP_C3 1
-#endif
                 else if (MBP_C3 && t == 3 && kStoreFrom == 3)
                     sc_span<D, false, false, CPT, true>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d, s_m1,
                                                         first, scale);
-                else
+                else if constexpr (!HOT)
                     sc_span<D, false, false, CPT>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d, s_m1, first,
                                                   scale);
-            } else {
+            } else if constexpr (!HOT) {
                 sc_span<D, true, false, CPT>(A, S, g, j0, r, r + span, t, act, lane, s_off, s_m, s_d, s_m1, first,
                                              scale);
             }
@@ -949,7 +961,7 @@ __device__ __forceinline__ int sc_compact(const ScatterArgs& A, int t, int gw, i
 // ---------------------------------------------------------------------------
 // one sweep t in a given layout
 // ---------------------------------------------------------------------------
-template <int D, bool CPT>
+template <int D, bool CPT, bool HOT>
 __device__ __forceinline__ void sc_sweep(const ScatterArgs& A, int G, int t, int& wc, int& ts_k, int lane, int nwarps,
                                          int* s_idx, unsigned* s_w, unsigned* s_x, unsigned* s_m, unsigned* s_v1m,
                                          uint8_t* s_v1d, int* s_mf, bool first, float scale, float iscale)
@@ -962,7 +974,7 @@ __device__ __forceinline__ void sc_sweep(const ScatterArgs& A, int G, int t, int
         const int total = G * A.C;
         const int ch = chunk_size(total, nwarps, CH);
         for (int base = claim(A.work + wc, lane, ch); base < total; base = claim(A.work + wc, lane, ch)) {
-            sc_check_chunk<D, CPT>(A, S, base, min(base + ch, total), t, cp, lane,
+            sc_check_chunk<D, CPT, HOT>(A, S, base, min(base + ch, total), t, cp, lane,
                                    reinterpret_cast<unsigned*>(s_idx), s_m, reinterpret_cast<int*>(s_x),
                                    reinterpret_cast<float*>(s_v1m), first, scale);
         }
@@ -1020,9 +1032,16 @@ __device__ __forceinline__ void sc_sweep(const ScatterArgs& A, int G, int t, int
     }
 }
 
-template <int D>
+// HOT = true: the hot instance (sweeps 1..kHotSweeps, clamp < sat).  When
+// frames remain undecided after sweep kHotSweeps it stores its loop state in
+// A.resume and exits; the full instance launched behind it (HOT = false,
+// A.resume set) resumes there, or returns at once when the flag is clear.
+// With A.resume == nullptr the full instance runs the whole decode.
+template <int D, bool HOT>
 __global__ void __launch_bounds__(kDecodeThreads, scatter_min_blocks<D>()) decode_scatter_kernel(const ScatterArgs A)
 {
+    const bool resumed = !HOT && A.resume;
+    if (resumed && ld_cg(A.resume) == 0) return;   // the hot instance finished the decode
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1071,54 +1090,81 @@ __global__ void __launch_bounds__(kDecodeThreads, scatter_min_blocks<D>()) decod
     bool may_compact = A.Gb > 0;
     int ts_k = 0;
     int wc = 0;
-    stamp(A, ts_k);
-
-    // fixed-point prior and sweep-1 magnitudes per frame
-    for (int f = gtid; f < A.G * 32; f += nthreads) {
-        A.Lfix[f] = __float2int_rn(A.Lmag[f] * scale);
-        for (int d = 0; d <= A.Dm; ++d)
-            A.Mfix[(size_t)d * A.G * 32 + f] = __float2int_rn(A.Mtab[(size_t)d * A.G * 32 + f] * scale);
-    }
-    // iteration 0: the uncorrected key against all u*m syndromes
-    // (_kernels.py:358-365); keeps the mismatch words for sweeps 1-3
-    {
-        const SL<false> S0{A, A.G};
-        const int total = A.G * cblk;
-        const int sc = syn_chunk(total, nwarps);
-        for (int base = claim(A.work + wc, lane, sc); base < total; base = claim(A.work + wc, lane, sc))
-            sc_syncheck_chunk<D, false>(A, S0, base, min(base + sc, total), 0, nullptr, cblk, lane);
-        ++wc;
-    }
-
     int t = 1;
-    int final_t = 0;
-    for (;; ++t) {
-        grid_barrier(A.barrier);
+    if (resumed) {
+        t = ld_cg(A.resume + 1);
+        cpt = ld_cg(A.resume + 2) != 0;
+        G = ld_cg(A.resume + 3);
+        tc = ld_cg(A.resume + 4);
+        may_compact = ld_cg(A.resume + 5) != 0;
+        wc = ld_cg(A.resume + 6);
+        ts_k = ld_cg(A.resume + 7);
+    } else {
         stamp(A, ts_k);
-        const int F = G * 32;
-        int* cnt = cpt ? A.cnt_b : A.cnt;
-        const int* cprev = cnt + ((t - 1) & 1) * F;
-        for (int f = gtid; f < F; f += nthreads) {
-            const int c = ld_cg(cprev + f);
-            const int fr = cpt ? ld_cg(A.fid_b + f) : f;
-            if (fr >= 0 && c == 0 && ld_cg(A.iters + fr) < 0) A.iters[fr] = t - 1;
-            cnt[(t & 1) * F + f] = 0;
-            if (may_compact) {
-                const unsigned msk = __ballot_sync(kFull, c != 0);
-                if (lane == 0) {
-                    A.grp_cnt[f >> 5] = __popc(msk);
-                    if (msk) {
-                        atomicAdd(A.ctrl + 2 * t, __popc(msk));
-                        atomicAdd(A.ctrl + 2 * t + 1, 1);
+
+        // fixed-point prior and sweep-1 magnitudes per frame
+        for (int f = gtid; f < A.G * 32; f += nthreads) {
+            A.Lfix[f] = __float2int_rn(A.Lmag[f] * scale);
+            for (int d = 0; d <= A.Dm; ++d)
+                A.Mfix[(size_t)d * A.G * 32 + f] = __float2int_rn(A.Mtab[(size_t)d * A.G * 32 + f] * scale);
+        }
+        // iteration 0: the uncorrected key against all u*m syndromes
+        // (_kernels.py:358-365); keeps the mismatch words for sweeps 1-3
+        {
+            const SL<false> S0{A, A.G};
+            const int total = A.G * cblk;
+            const int sc = syn_chunk(total, nwarps);
+            for (int base = claim(A.work + wc, lane, sc); base < total; base = claim(A.work + wc, lane, sc))
+                sc_syncheck_chunk<D, false>(A, S0, base, min(base + sc, total), 0, nullptr, cblk, lane);
+            ++wc;
+        }
+    }
+
+    int final_t = 0;
+    bool top = !resumed;   // the resumed sweep's loop-top bookkeeping ran in the hot instance
+    for (;; ++t) {
+        if (top) {
+            grid_barrier(A.barrier);
+            stamp(A, ts_k);
+            const int F = G * 32;
+            int* cnt = cpt ? A.cnt_b : A.cnt;
+            const int* cprev = cnt + ((t - 1) & 1) * F;
+            for (int f = gtid; f < F; f += nthreads) {
+                const int c = ld_cg(cprev + f);
+                const int fr = cpt ? ld_cg(A.fid_b + f) : f;
+                if (fr >= 0 && c == 0 && ld_cg(A.iters + fr) < 0) A.iters[fr] = t - 1;
+                cnt[(t & 1) * F + f] = 0;
+                if (may_compact) {
+                    const unsigned msk = __ballot_sync(kFull, c != 0);
+                    if (lane == 0) {
+                        A.grp_cnt[f >> 5] = __popc(msk);
+                        if (msk) {
+                            atomicAdd(A.ctrl + 2 * t, __popc(msk));
+                            atomicAdd(A.ctrl + 2 * t + 1, 1);
+                        }
                     }
                 }
             }
+            if (ld_cg(A.any_bad + ((t - 1) & 1)) == 0 || t > A.max_it) {
+                final_t = t - 1;
+                break;
+            }
+            if (gtid == 0) A.any_bad[t & 1] = 0;
+            if (HOT && t > kHotSweeps) {
+                if (gtid == 0) {
+                    A.resume[1] = t;
+                    A.resume[2] = cpt;
+                    A.resume[3] = G;
+                    A.resume[4] = tc;
+                    A.resume[5] = may_compact;
+                    A.resume[6] = wc;
+                    A.resume[7] = ts_k;
+                    A.resume[0] = 1;
+                }
+                return;
+            }
         }
-        if (ld_cg(A.any_bad + ((t - 1) & 1)) == 0 || t > A.max_it) {
-            final_t = t - 1;
-            break;
-        }
-        if (gtid == 0) A.any_bad[t & 1] = 0;
+        top = true;
         if (may_compact && t >= 2) {
             grid_barrier(A.barrier);
             const int nund = ld_cg(A.ctrl + 2 * t);
@@ -1132,11 +1178,11 @@ __global__ void __launch_bounds__(kDecodeThreads, scatter_min_blocks<D>()) decod
             }
         }
         if (cpt)
-            sc_sweep<D, true>(A, G, t, wc, ts_k, lane, nwarps, s_idx, s_w, s_x, s_m, s_v1m, s_v1d, s_mf, t == tc,
-                              scale, iscale);
+            sc_sweep<D, true, HOT>(A, G, t, wc, ts_k, lane, nwarps, s_idx, s_w, s_x, s_m, s_v1m, s_v1d, s_mf, t == tc,
+                                   scale, iscale);
         else
-            sc_sweep<D, false>(A, G, t, wc, ts_k, lane, nwarps, s_idx, s_w, s_x, s_m, s_v1m, s_v1d, s_mf, false,
-                               scale, iscale);
+            sc_sweep<D, false, HOT>(A, G, t, wc, ts_k, lane, nwarps, s_idx, s_w, s_x, s_m, s_v1m, s_v1d, s_mf, false,
+                                    scale, iscale);
     }
 
     if (cpt) grid_barrier(A.barrier);
