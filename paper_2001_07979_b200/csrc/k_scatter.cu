@@ -6,10 +6,8 @@
 
 namespace mbp {
 
-#define MBP_SC(DD) case DD: return launch_coop(decode_scatter_kernel<DD, false>, A, sm, s);
-#define MBP_SCH(DD) \
-    case DD: return hot ? launch_coop(decode_scatter_kernel<DD, true>, A, sm, s) \
-                        : launch_coop(decode_scatter_kernel<DD, false>, A, sm, s);
+#define MBP_SC(DD) case DD: return launch_scatter<DD, false>(A, sm, s);
+#define MBP_SCH(DD) case DD: return hot ? launch_scatter<DD, true>(A, sm, s) : launch_scatter<DD, false>(A, sm, s);
 
 #if MBP_SCATTER_PART == 0
 cudaError_t launch_scatter_small(const ScatterArgs& A, int D, bool hot, int sm, cudaStream_t s)

@@ -21,15 +21,26 @@ cudaError_t launch_scatter_small(const ScatterArgs& A, int D, bool hot, int sm_c
 cudaError_t launch_scatter_mid(const ScatterArgs& A, int D, bool hot, int sm_count, cudaStream_t s);     // D 9..16
 cudaError_t launch_scatter_large(const ScatterArgs& A, int D, int sm_count, cudaStream_t s);             // D 20..64
 
+// smem: dynamic shared memory per block (opted in above 48 KB)
 template <class Kern, class Args>
-cudaError_t launch_coop(Kern kern, const Args& A, int sm_count, cudaStream_t s)
+cudaError_t launch_coop(Kern kern, const Args& A, int sm_count, cudaStream_t s, size_t smem = 0)
 {
+    cudaError_t err;
+    if (smem > 48 * 1024 &&
+        (err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+        return err;
     int per_sm = 0;
-    cudaError_t err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDecodeThreads, 0);
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDecodeThreads, smem);
     if (err != cudaSuccess) return err;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     void* args[] = {(void*)&A};
-    return cudaLaunchCooperativeKernel((const void*)kern, dim3(per_sm * sm_count), dim3(kDecodeThreads), args, 0, s);
+    return cudaLaunchCooperativeKernel((const void*)kern, dim3(per_sm * sm_count), dim3(kDecodeThreads), args, smem, s);
+}
+
+template <int D, bool HOT>
+cudaError_t launch_scatter(const ScatterArgs& A, int sm_count, cudaStream_t s)
+{
+    return launch_coop(decode_scatter_kernel<D, HOT>, A, sm_count, s, ScatterSmem<D>::bytes);
 }
 
 }  // namespace mbp

@@ -1032,6 +1032,27 @@ __device__ __forceinline__ void sc_sweep(const ScatterArgs& A, int G, int t, int
     }
 }
 
+// Per-warp shared-memory carve-out of decode_scatter_kernel, in 32-bit words
+// (one contiguous slice per warp, dynamic shared memory; measured against the
+// per-array static layout it replaced: sweep-1 variable phase 0.219 ->
+// 0.201 ms, cfg 2 kernel 1.375 -> 1.342 ms):
+//   idx  check phases: row variable offsets [CH][SD]; sweep 1: Mfix table
+//   w, x, m  [CH] staging words
+//   raw  sweep-1 staging (regular column degree 6 or 9, check degree <= 16:
+//        mismatch words + degrees + per-variable uniform degree) or, in
+//        check phases, the lane's sweep-1 magnitude per degree
+template <int D> struct ScatterSmem {
+    static constexpr int CH = Chunk<D>::CH;
+    static constexpr int MF = D <= 16 ? (D + 1) * 32 : 1;
+    static constexpr int kSlice = CH * Chunk<D>::SD > MF ? CH * Chunk<D>::SD : MF;
+    static constexpr int kCH = CH > 32 ? CH : 32;
+    static constexpr int kV1 = D <= 16 ? 32 * 9 : 0;
+    static constexpr int M1T = D <= 16 ? (D + 1) * 32 : 0;
+    static constexpr int kRaw = (kV1 + kV1 / 4 + 8) > M1T ? (kV1 + kV1 / 4 + 8) + 1 : M1T + 1;
+    static constexpr int kWarp = (kSlice + 3 * kCH + kRaw + 1) & ~1;
+    static constexpr size_t bytes = (size_t)(kDecodeThreads / 32) * kWarp * 4;
+};
+
 // HOT = true: the hot instance (sweeps 1..kHotSweeps, clamp < sat).  When
 // frames remain undecided after sweep kHotSweeps it stores its loop state in
 // A.resume and exits; the full instance launched behind it (HOT = false,
@@ -1049,26 +1070,15 @@ __global__ void __launch_bounds__(kDecodeThreads, scatter_min_blocks<D>()) decod
     const int nwarps = nthreads >> 5;
     const int gw = gtid >> 5;
     const int cblk = (A.C + 31) / 32;
-    constexpr int CH = Chunk<D>::CH;
-    constexpr int MF = D <= 16 ? (D + 1) * 32 : 1;                 // sweep-1 Mfix table (aliases s_idx)
-    constexpr int SLICE = CH * Chunk<D>::SD > MF ? CH * Chunk<D>::SD : MF;
-    __shared__ int s_idx_all[kDecodeThreads / 32][SLICE];
-    __shared__ unsigned s_w_all[kDecodeThreads / 32][CH > 32 ? CH : 32];
-    __shared__ unsigned s_x_all[kDecodeThreads / 32][CH > 32 ? CH : 32];
-    __shared__ unsigned s_m_all[kDecodeThreads / 32][CH > 32 ? CH : 32];
-    // per-warp scratch: sweep-1 staging (regular column degree 6 or 9, check
-    // degree <= 16: mismatch words + degrees) or, in check phases, the
-    // lane's sweep-1 magnitude per degree
-    constexpr int V1 = D <= 16 ? 32 * 9 : 0;
-    constexpr int M1T = D <= 16 ? (D + 1) * 32 : 0;
-    constexpr int RAW = (V1 + V1 / 4 + 8) > M1T ? (V1 + V1 / 4 + 8) + 1 : M1T + 1;   // + per-variable uniform degree
-    __shared__ unsigned s_raw_all[kDecodeThreads / 32][RAW];
-    int* s_idx = s_idx_all[warp];
-    unsigned* s_w = s_w_all[warp];
-    unsigned* s_x = s_x_all[warp];
-    unsigned* s_m = s_m_all[warp];
-    unsigned* s_v1m = s_raw_all[warp];
-    uint8_t* s_v1d = reinterpret_cast<uint8_t*>(s_raw_all[warp] + V1);
+    using SM = ScatterSmem<D>;
+    extern __shared__ __align__(16) unsigned s_dyn[];   // SM::bytes, set by launch_scatter
+    unsigned* s_warp = s_dyn + warp * SM::kWarp;
+    int* s_idx = reinterpret_cast<int*>(s_warp);
+    unsigned* s_w = s_warp + SM::kSlice;
+    unsigned* s_x = s_w + SM::kCH;
+    unsigned* s_m = s_x + SM::kCH;
+    unsigned* s_v1m = s_m + SM::kCH;
+    uint8_t* s_v1d = reinterpret_cast<uint8_t*>(s_v1m + SM::kV1);
     int* s_mf = s_idx;   // only used in the sweep-1 variable phase
 
     // fixed-point scale: |acc| <= Lmax + dv_max * clamp (+ rounding) < 2^30
