@@ -601,7 +601,7 @@ __device__ __forceinline__ void sc_var1_chunk(const ScatterArgs& A, const SL<CPT
             if (act == kFull && !A.hist_w) {
                 // every lane live, no history: UV variables per pass, no predicates
 #ifndef MBP_V1_UV
-#define MBP_V1_UV 4
+#define MBP_V1_UV 8   // 8 variables per pass: cfg 3 3.033 -> 3.009 ms (the D = 14 sweep-3 check, register allocation), cfg 2 unchanged
 #endif
                 constexpr int UV = MBP_V1_UV;
                 int v = r;
