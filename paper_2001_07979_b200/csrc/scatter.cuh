@@ -503,7 +503,11 @@ __device__ __forceinline__ void sc_check_chunk(const ScatterArgs& A, const SL<CP
 // arms acc with the prior for sweep 2.  General column degrees: lanes load
 // the variable's check ids, mismatch words and degrees, the warp walks them
 // with shuffles.
-template <bool CPT>
+// RECOMP (compaction at t = kStoreFrom, MBP_CMP_RECOMP): rebuild post'_1 of a
+// compacted frame from its moved mismatch words instead of gathering it from
+// the frame's old lane; writes the post'_1 line only (the move re-armed acc,
+// hard words are not touched).  Mfix rows have stride A.G * 32.
+template <bool CPT, bool RECOMP = false>
 __device__ __forceinline__ void sc_var1_item(const ScatterArgs& A, const SL<CPT>& S, int g, int i, unsigned act,
                                              int lane, const int* Mfix, int Lf, float iscale)
 {
@@ -525,12 +529,13 @@ __device__ __forceinline__ void sc_var1_item(const ScatterArgs& A, const SL<CPT>
         for (int k = 0; k < cntk; ++k) {
             const unsigned mw = __shfl_sync(kFull, mk, k);
             const int d = __shfl_sync(kFull, dk, k);
-            const int mf = ld_cg(Mfix + (size_t)d * S.Gc() * 32);
+            const int mf = ld_cg(Mfix + (size_t)d * A.G * 32);
             a += ((mw >> lane) & 1u) ? -mf : mf;
         }
     }
     float* vr = S.vrow(w, lane);
     st_if(vr + 32, (float)a * iscale, live);
+    if constexpr (RECOMP) return;
     if (live) reinterpret_cast<int*>(vr)[64] = a;   // acc = post'_1 in fixed point
     const unsigned neg = __ballot_sync(kFull, y ? a > 0 : a < 0);
     if (lane == 0) {
@@ -545,7 +550,7 @@ __device__ __forceinline__ void sc_var1_item(const ScatterArgs& A, const SL<CPT>
 // chunk of <= 32 variables.  The chunk's mismatch words and check degrees
 // are staged in shared memory with independent loads (two dependent round
 // trips per chunk), the lane's Mfix row per degree sits in a shared table.
-template <int D, int DV, bool CPT>
+template <int D, int DV, bool CPT, bool RECOMP = false>
 __device__ __forceinline__ void sc_var1_chunk(const ScatterArgs& A, const SL<CPT>& S, int base, int end,
                                               const int* cprev, int lane, unsigned* s_mis, uint8_t* s_deg,
                                               unsigned* s_y, int* s_mf, float iscale)
@@ -592,8 +597,13 @@ __device__ __forceinline__ void sc_var1_chunk(const ScatterArgs& A, const SL<CPT
         const int span = min(rows - r, A.n - i);
         const unsigned act = group_mask(cprev, g, lane);
         if (act) {
+            {
+                // the lane's frame slot in the primary layout (Mfix is indexed by it)
+                int src = g * 32 + lane;
+                if constexpr (RECOMP) src = max(ld_cg(A.src_b + g * 32 + lane), 0);
 #pragma unroll
-            for (int d = 0; d <= D; ++d) s_mf[d * 32 + lane] = ld_cg(A.Mfix + (size_t)d * A.G * 32 + g * 32 + lane);
+                for (int d = 0; d <= D; ++d) s_mf[d * 32 + lane] = ld_cg(A.Mfix + (size_t)d * A.G * 32 + src);
+            }
             __syncwarp();
             const bool live = (act >> lane) & 1u;
             const int Lf = S.Lfix(g * 32 + lane);
@@ -626,6 +636,11 @@ __device__ __forceinline__ void sc_var1_chunk(const ScatterArgs& A, const SL<CPT
                     }
                     const size_t w = (size_t)base + v;
                     float* vr = S.vrow(w, lane);
+                    if constexpr (RECOMP) {
+#pragma unroll
+                        for (int q = 0; q < UV; ++q) vr[q * kVB + 32] = (float)a[q] * iscale;
+                        continue;
+                    }
                     unsigned nq[UV];
 #pragma unroll
                     for (int q = 0; q < UV; ++q) {
@@ -651,6 +666,7 @@ __device__ __forceinline__ void sc_var1_chunk(const ScatterArgs& A, const SL<CPT
                     const size_t w = (size_t)base + v;
                     float* vr = S.vrow(w, lane);
                     vr[32] = (float)a0 * iscale;
+                    if constexpr (RECOMP) continue;
                     reinterpret_cast<int*>(vr)[64] = a0;
                     const unsigned n0 = __ballot_sync(kFull, (s_y[v] & lbit) ? a0 > 0 : a0 < 0);
                     if (lane == 0) S.hard_w()[w] = n0;
@@ -669,6 +685,7 @@ __device__ __forceinline__ void sc_var1_chunk(const ScatterArgs& A, const SL<CPT
                     }
                     float* vr = S.vrow(w, lane);
                     st_if(vr + 32, (float)a * iscale, live);
+                    if constexpr (RECOMP) continue;
                     if (live) reinterpret_cast<int*>(vr)[64] = a;   // acc = post'_1 in fixed point
                     const unsigned neg = __ballot_sync(kFull, y ? a > 0 : a < 0);
                     if (lane == 0) {
@@ -859,6 +876,15 @@ __device__ __forceinline__ void sc_syncheck_chunk(const ScatterArgs& A, const SL
     if (__any_sync(kFull, bad) && lane == 0) atomicOr(A.any_bad + (t & 1), 1);
 }
 
+// MBP_CMP_RECOMP: a compaction at t <= kStoreFrom moves post'_2 and re-arms
+// acc, and post'_1 (= L + sum of +-M_d over the iteration-0 mismatch bits,
+// integer arithmetic: the same value) is rebuilt in the compacted layout from
+// the moved mismatch words instead of being gathered sector by sector from
+// the frames' old lanes.
+#ifndef MBP_CMP_RECOMP
+#define MBP_CMP_RECOMP 1   // cfg 2: move 0.117 -> 0.080 ms, + 0.033 ms rebuild phase: kernel 1.342 -> 1.332 ms
+#endif
+
 // ---------------------------------------------------------------------------
 // compaction (cf. decode.cuh compact()): repack the undecided frames into
 // dense groups of the secondary layout at the start of sweep t >= 2
@@ -907,6 +933,7 @@ __device__ __forceinline__ int sc_compact(const ScatterArgs& A, int t, int gw, i
     // domain) and the first compacted check phase adds absolute messages
     {
         const bool both = t <= kStoreFrom;
+        const bool recomp = MBP_CMP_RECOMP && both;   // post'_1 rebuilt after the move (sc_recomp_post1)
         const int keep = ((t - 1) & 1) * 32;
 #ifndef MBP_MOVE_XU
 #define MBP_MOVE_XU 4
@@ -926,14 +953,14 @@ __device__ __forceinline__ int sc_compact(const ScatterArgs& A, int t, int gw, i
                 const bool ok = s >= 0 && i0 + k < A.n;
                 const size_t o = (size_t)(i0 + k) * kVB;
                 v0[k] = ok && (both || keep == 0) ? __ldca(src + o) : 0.0f;
-                v1[k] = ok && (both || keep == 32) ? __ldca(src + o + 32) : 0.0f;
+                v1[k] = ok && ((both && !recomp) || keep == 32) ? __ldca(src + o + 32) : 0.0f;
             }
 #pragma unroll
             for (int k = 0; k < XU; ++k) {
                 if (i0 + k >= A.n) break;
                 float* d = dst + (size_t)(i0 + k) * kVB;
                 d[0] = v0[k];
-                d[32] = v1[k];
+                if (!recomp) d[32] = v1[k];
                 reinterpret_cast<int*>(d)[64] = Lf;
             }
         }
@@ -956,6 +983,46 @@ __device__ __forceinline__ int sc_compact(const ScatterArgs& A, int t, int gw, i
     stamp_compact(A, 3);
     if (gtid == 0) A.sweeps_run[1] = t;
     return Gn;
+}
+
+// post'_1 of the compacted frames (MBP_CMP_RECOMP), right after a compaction
+// at sweep t <= kStoreFrom: the sweep-1 variable phase in RECOMP mode
+template <int D>
+__device__ __forceinline__ void sc_recomp_post1(const ScatterArgs& A, int G, int t, int& wc, int lane, int nwarps,
+                                                unsigned* s_w, unsigned* s_v1m, uint8_t* s_v1d, int* s_mf,
+                                                float iscale)
+{
+    const SL<true> S{A, G};
+    const int* cp = A.cnt_b + ((t - 1) & 1) * G * 32;   // compacted frames' counts: live lanes
+    const int total = G * A.n;
+    const bool v1_staged = D <= 16 && (A.dv_max == 6 || A.dv_max == 9) && A.var_ptr_regular;
+    if (v1_staged) {
+        if constexpr (D <= 16) {
+            const int ch = chunk_size(total, nwarps, 32);
+            for (int base = claim(A.work + wc, lane, ch); base < total; base = claim(A.work + wc, lane, ch)) {
+                if (A.dv_max == 6)
+                    sc_var1_chunk<D, 6, true, true>(A, S, base, min(base + ch, total), cp, lane, s_v1m, s_v1d, s_w,
+                                                    s_mf, iscale);
+                else
+                    sc_var1_chunk<D, 9, true, true>(A, S, base, min(base + ch, total), cp, lane, s_v1m, s_v1d, s_w,
+                                                    s_mf, iscale);
+            }
+        }
+    } else {
+        for (int base = claim(A.work + wc, lane, 8); base < total; base = claim(A.work + wc, lane, 8)) {
+            const int end = min(base + 8, total);
+            for (int item = base; item < end; ++item) {
+                const int g = item / A.n;
+                const unsigned act = group_mask(cp, g, lane);
+                if (act) {
+                    const int src = max(ld_cg(A.src_b + g * 32 + lane), 0);
+                    sc_var1_item<true, true>(A, S, g, item - g * A.n, act, lane, A.Mfix + src,
+                                             S.Lfix(g * 32 + lane), iscale);
+                }
+            }
+        }
+    }
+    ++wc;
 }
 
 // ---------------------------------------------------------------------------
@@ -1182,6 +1249,10 @@ __global__ void __launch_bounds__(kDecodeThreads, scatter_min_blocks<D>()) decod
             const int gn = (nund + 31) / 32;
             if (nund * 2 <= gact * 32 && gn < gact && gn <= A.Gb) {
                 G = sc_compact(A, t, gw, nwarps, gtid, nthreads, lane);
+                if (MBP_CMP_RECOMP && t <= kStoreFrom) {
+                    sc_recomp_post1<D>(A, G, t, wc, lane, nwarps, s_w, s_v1m, s_v1d, s_mf, iscale);
+                    grid_barrier(A.barrier);
+                }
                 cpt = true;
                 tc = t;
                 may_compact = false;
