@@ -884,6 +884,12 @@ __device__ __forceinline__ void sc_syncheck_chunk(const ScatterArgs& A, const SL
 #ifndef MBP_CMP_RECOMP
 #define MBP_CMP_RECOMP 1   // cfg 2: move 0.117 -> 0.080 ms, + 0.033 ms rebuild phase: kernel 1.342 -> 1.332 ms
 #endif
+// short keys: the rebuild phase's fixed cost (a claimed phase + a grid
+// barrier) exceeds the sectors it saves (cfg 1, n = 4096: +0.01 ms)
+__device__ __forceinline__ bool cmp_recomp(const ScatterArgs& A, int t)
+{
+    return MBP_CMP_RECOMP && t <= kStoreFrom && A.n >= 16384;
+}
 
 // ---------------------------------------------------------------------------
 // compaction (cf. decode.cuh compact()): repack the undecided frames into
@@ -933,7 +939,7 @@ __device__ __forceinline__ int sc_compact(const ScatterArgs& A, int t, int gw, i
     // domain) and the first compacted check phase adds absolute messages
     {
         const bool both = t <= kStoreFrom;
-        const bool recomp = MBP_CMP_RECOMP && both;   // post'_1 rebuilt after the move (sc_recomp_post1)
+        const bool recomp = cmp_recomp(A, t);   // post'_1 rebuilt after the move (sc_recomp_post1)
         const int keep = ((t - 1) & 1) * 32;
 #ifndef MBP_MOVE_XU
 #define MBP_MOVE_XU 4
@@ -1249,7 +1255,7 @@ __global__ void __launch_bounds__(kDecodeThreads, scatter_min_blocks<D>()) decod
             const int gn = (nund + 31) / 32;
             if (nund * 2 <= gact * 32 && gn < gact && gn <= A.Gb) {
                 G = sc_compact(A, t, gw, nwarps, gtid, nthreads, lane);
-                if (MBP_CMP_RECOMP && t <= kStoreFrom) {
+                if (cmp_recomp(A, t)) {
                     sc_recomp_post1<D>(A, G, t, wc, lane, nwarps, s_w, s_v1m, s_v1d, s_mf, iscale);
                     grid_barrier(A.barrier);
                 }
