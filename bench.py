@@ -180,6 +180,7 @@ class ClockSampler:
         self.gpu = gpu_index
         self.samples = []   # (sm_mhz, max_mhz, reasons bitmask)
         self._stop = threading.Event()
+        self._ready = threading.Event()   # set after the first sample (or a failed init)
         self._t = None
         self.source = "nvml"
 
@@ -189,6 +190,7 @@ class ClockSampler:
         while not self._stop.is_set():
             self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), mx,
                                  nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+            self._ready.set()
             self._stop.wait(0.001)
 
     def _run_smi(self):
@@ -205,6 +207,8 @@ class ClockSampler:
                 self.samples.append((float(v[0]), float(v[1]), mask))
             except Exception:
                 return
+            finally:
+                self._ready.set()
             self._stop.wait(0.05)
 
     def _run(self):
@@ -217,12 +221,15 @@ class ClockSampler:
         try:
             self._run_nvml(nv)
         finally:
+            self._ready.set()
             nv.nvmlShutdown()
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
-        time.sleep(0.005)   # first sample before the timed region
+        # NVML init can take longer than a short timed region: wait for the
+        # first sample so that the region is always sampled
+        self._ready.wait(timeout=10)
         return self
 
     def __exit__(self, *a):
