@@ -310,3 +310,37 @@ def test_phase_timers_account_for_the_compaction(cfg2_ensemble):
     ref = BatchDecoder(cfg2_ensemble, B).decode_device(torch.from_numpy(fb.noisy).to(dev), syn, 0.03)
     for a, b in zip(out, ref):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("mix", [False, True])
+def test_compaction_rebuild_of_post1_is_transparent(cfg2_ensemble, mix):
+    """n >= 16384: a compaction at the start of sweep 3 rebuilds post'_1 in
+    the compacted layout from the moved mismatch words instead of moving it
+    (scatter.cuh sc_recomp_post1); every output must equal the uncompacted
+    decode's.  mix: every fourth frame at e = 0.065 (sweeps 4+ after the
+    compaction, on the explicit base), per-frame crossover probabilities."""
+    B = 512
+    if mix:
+        # every fourth frame at e = 0.065: each 32-frame group is mostly
+        # decided after sweep 2, so the decode compacts at sweep 3
+        fa = make_frames(cfg2_ensemble.n, 0.025, 3 * B // 4, seed=21)
+        fb = make_frames(cfg2_ensemble.n, 0.065, B // 4, seed=22)
+        hard = np.arange(B) % 4 == 3
+        keys = np.empty((B,) + fa.keys.shape[1:], fa.keys.dtype)
+        noisy = np.empty((B,) + fa.noisy.shape[1:], fa.noisy.dtype)
+        keys[~hard], keys[hard], noisy[~hard], noisy[hard] = fa.keys, fb.keys, fa.noisy, fb.noisy
+        e = np.where(hard, 0.065, 0.025)
+    else:
+        fa = make_frames(cfg2_ensemble.n, 0.03, B, seed=21)
+        keys, noisy, e = fa.keys, fa.noisy, 0.03
+    on = BatchDecoder(cfg2_ensemble, B)
+    off = BatchDecoder(cfg2_ensemble, B, flags=N.MBP_NO_COMPACTION)
+    syn = on.syndromes(keys)
+    a = on.decode(noisy, syn, e)
+    assert on.last_stats()[1] == 3, on.last_stats()   # compacted at the start of sweep 3
+    b = off.decode(noisy, syn, e)
+    assert off.last_stats()[1] == 0
+    for f in ("corrected", "converged", "iterations", "mismatches"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
+    if mix:
+        assert a.iterations.max() >= 4
